@@ -1,0 +1,147 @@
+/* hgks_b200 — C ABI of the B200-native DG-HGKS time step.
+ *
+ * The drop-in boundary: plain pointers and sizes, no torch or CUDA types.
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj/include/hgks/). The C++ host
+ * header include/hgks_b200/hgks.hpp wraps these in the reference's own
+ * hgks:: names and exception types; INTEGRATION.md shows the bindings.
+ *
+ * Host layouts are the reference's: coefficients AoS [(cell*N + n)*5 + var]
+ * (dg.hpp:15-17, cell = i + nx*(j + ny*k), mesh.hpp:34); face buffers
+ * [face*(npts*10) + p*10 + (F|Ft)] (dg.hpp:287). The device keeps SoA
+ * [n*5+var][cell] with one ghost cell layer above and below in z.
+ *
+ * Return codes: HGKS_OK, or
+ *   HGKS_ERR_STATE   invalid_state_error: non-positive density / pressure
+ *                    (core.hpp:58-70), message "item <i>: non-positive ..."
+ *                    exactly as worker_error shapes it (runtime.hpp:37-41)
+ *   HGKS_ERR_CONFIG  std::invalid_argument-class configuration error
+ *   HGKS_ERR_DT      non_positive_dt (integrator.hpp:17-19, :43)
+ *   HGKS_ERR_CUDA    CUDA runtime failure (no CPU fallback exists)
+ * hgks_last_error() returns the message of the most recent failure.
+ */
+#ifndef HGKS_B200_H
+#define HGKS_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HGKS_OK 0
+#define HGKS_ERR_STATE 1
+#define HGKS_ERR_CONFIG 2
+#define HGKS_ERR_DT 3
+#define HGKS_ERR_CUDA 4
+
+#define HGKS_ABI_VERSION 1
+
+typedef struct hgks_solver hgks_solver;
+
+/* Mesh + Scheme (mesh.hpp:11-30, dg.hpp:269-281, core.hpp:35-42). */
+typedef struct {
+    int nx, ny, nz;                  /* global cells per axis */
+    const double* xs;                /* nx+1 node coordinates, strictly increasing */
+    const double* ys;                /* ny+1 */
+    const double* zs;                /* nz+1 */
+    int degree;                      /* 2 or 3 (reference); 1 = P1 extension */
+    int dim;                         /* 3 (2 = degenerate 2D mode, nz must be 1) */
+    double gamma;                    /* GasModel::make gamma */
+    double mu;                       /* mu_ref = 1/Re; 0 selects the Euler (tau = 0) limit */
+    int device;                      /* CUDA device ordinal */
+    int z_begin, z_count;            /* owned z-slab [z_begin, z_begin+z_count); z_count<=0: all */
+} hgks_config;
+
+int hgks_abi_version(void);
+
+/* Creates the solver on cfg->device. Scheme::make + ResidualWorkspace::resize
+ * + TwoStageScratch in one object (dg.hpp:274, :294; integrator.hpp:50). */
+int hgks_create(const hgks_config* cfg, hgks_solver** out);
+void hgks_destroy(hgks_solver* s);
+const char* hgks_last_error(const hgks_solver* s);
+/* structured form of the last failure: code, phase (0 face, 1 cell, 2 dt),
+ * reference item index, offending value */
+void hgks_error_info(const hgks_solver* s, int* code, int* phase, long* item, double* value);
+
+int hgks_num_basis(const hgks_solver* s);      /* BasisSet::N (basis.hpp:64-82) */
+long hgks_num_coeffs(const hgks_solver* s);    /* owned cells * N * 5 */
+int hgks_face_points(const hgks_solver* s, int axis); /* face_minus[axis].npts */
+
+/* DGState coefficients (dg.hpp:18-38) of the owned cells, host AoS. */
+int hgks_set_state(hgks_solver* s, const double* coeffs, double time);
+int hgks_get_state(hgks_solver* s, double* coeffs, double* time);
+
+/* residual(coeffs, mesh, scheme, dt, ws) (dg.hpp:354-450): R, Rt as ws.R /
+ * ws.Rt; face0..2 (optional, may be NULL) as ws.face[a]. coeffs may be NULL
+ * to use the current state. */
+int hgks_residual(hgks_solver* s, const double* coeffs, double dt, double* R, double* Rt,
+                  double* face0, double* face1, double* face2);
+
+/* detail::apply_inverse_mass(R, L, mesh, basis, part) (solver.hpp:42-54) */
+int hgks_apply_inverse_mass(hgks_solver* s, const double* R, double* L);
+
+/* compute_dt(state, mesh, gas, ctrl, degree) (integrator.hpp:27-45) on the
+ * current state, ctrl.cfl = cfl. */
+int hgks_compute_dt(hgks_solver* s, double cfl, double* dt);
+
+/* two_stage_step(q, dt, eval, scratch) (integrator.hpp:64-75) with the eval
+ * of solver.hpp:81-88 (residual + inverse mass, the same full dt in both
+ * stages), applied to the device-resident state; state time += dt.
+ * On failure the state is left unchanged. */
+int hgks_step(hgks_solver* s, double dt);
+
+/* The same step on a caller-owned host vector q (AoS, hgks_num_coeffs):
+ * host->device, step, device->host. The literal drop-in for
+ * two_stage_step(r.state.coeffs, dt, eval, scratch). */
+int hgks_two_stage_step_host(hgks_solver* s, double* q, double dt);
+
+/* advance() (solver.hpp:62-108) without records: steps from the current time
+ * to t_end with dt = compute_dt (cfl) or dt_fixed (> 0), clipped to t_end and
+ * to multiples of record_interval (> 0 only). Writes the number of steps taken. */
+int hgks_advance(hgks_solver* s, double t_end, double cfl, double dt_fixed,
+                 double record_interval, int* steps);
+
+/* ResidualWorkspace::count_fluxes debug tally (dg.hpp:291-292, :393): counts
+ * owned face-point flux evaluations. */
+void hgks_set_count_fluxes(hgks_solver* s, int on);
+long hgks_flux_evaluations(const hgks_solver* s);
+
+/* project(initial_field(cfg)) (dg.hpp:193-220, cases.hpp:127-137) on the
+ * device: case_name adv2d | adv3d | vortex2d | tgv (gamma 1.4, Ma 0.1,
+ * eps 5 as CaseConfig::named, cases.hpp:12-46); exact field at time t. */
+int hgks_project_case(hgks_solver* s, const char* case_name, double t);
+
+/* tgv_diagnostics (cases.hpp:165-204) of the current state: Ek, epsZeta
+ * (fixed-order device reduction; sums over owned cells only). */
+int hgks_tgv_diagnostics(hgks_solver* s, double* ek_vol, double* ens_vol, double* volume);
+
+/* ---- multi-GPU z-slabs. The halo is one layer of cell
+ * coefficients below and above the owned slab. */
+/* device pointers (as integers) and byte size of the owned bottom / top
+ * layers (send) and ghost bottom / top layers (receive) of the array that is
+ * the input of the next residual; valid until the next call. */
+int hgks_halo_buffers(hgks_solver* s, unsigned long long* send_lo, unsigned long long* send_hi,
+                      unsigned long long* recv_lo, unsigned long long* recv_hi,
+                      long* layer_bytes, long* comp_stride_bytes, int* ncomp);
+/* callback run at each exchange point, on the solver's stream; returns 0 on
+ * success. Without one, ghosts are filled by the periodic wrap (single slab). */
+typedef int (*hgks_halo_fn)(void* user, hgks_solver* s);
+void hgks_set_halo_exchange(hgks_solver* s, hgks_halo_fn fn, void* user);
+/* dt reduction hook for multi-slab runs: min over ranks (order independent). */
+typedef int (*hgks_min_fn)(void* user, double* value);
+void hgks_set_dt_reduce(hgks_solver* s, hgks_min_fn fn, void* user);
+
+/* ---- runtime plumbing */
+int hgks_set_stream(hgks_solver* s, void* cuda_stream); /* NULL = solver-owned stream */
+void* hgks_get_stream(hgks_solver* s);
+int hgks_synchronize(hgks_solver* s);
+/* kernel launches issued by this solver so far (for the bench's gpu_launches) */
+long hgks_launch_count(const hgks_solver* s);
+/* duration in ms of the last hgks_step's face and cell kernels (CUDA events on
+ * the solver stream) when timing is enabled */
+void hgks_set_kernel_timing(hgks_solver* s, int on);
+int hgks_kernel_times(hgks_solver* s, double* face_ms, double* cell_ms, double* other_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,311 @@
+// Auxiliary device kernels: AoS<->SoA transforms at the ABI, inverse mass
+// matrix, L2 projection of the case fields (dg.hpp:193-220, cases.hpp:78-137)
+// and the Taylor-Green diagnostics (cases.hpp:165-204).
+#pragma once
+
+#include "hgks_kernels.cuh"
+
+namespace hgks_dev {
+
+// host AoS [(c*NC) + comp] (owned cells) <-> device SoA comp*cs + S + c.
+// 32 cells per block, staged through shared memory so both sides coalesce.
+__global__ void aos_to_soa_kernel(KParams kp, const double* __restrict__ aos,
+                                  double* __restrict__ soa, int NC) {
+    __shared__ double st[100 * 33];
+    const long ncell = (long)kp.S * kp.nzl;
+    for (long c0 = (long)blockIdx.x * 32; c0 < ncell; c0 += (long)gridDim.x * 32) {
+        const int nc = (int)min(32L, ncell - c0);
+        for (int e = threadIdx.x; e < nc * NC; e += blockDim.x) {
+            const int l = e / NC, comp = e - l * NC;
+            st[comp * 33 + l] = aos[c0 * NC + e];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < 32 * NC; e += blockDim.x) {
+            const int l = e & 31, comp = e >> 5;
+            if (l < nc) soa[comp * kp.cs + kp.S + c0 + l] = st[comp * 33 + l];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void soa_to_aos_kernel(KParams kp, const double* __restrict__ soa,
+                                  double* __restrict__ aos, int NC) {
+    __shared__ double st[100 * 33];
+    const long ncell = (long)kp.S * kp.nzl;
+    for (long c0 = (long)blockIdx.x * 32; c0 < ncell; c0 += (long)gridDim.x * 32) {
+        const int nc = (int)min(32L, ncell - c0);
+        for (int e = threadIdx.x; e < 32 * NC; e += blockDim.x) {
+            const int l = e & 31, comp = e >> 5;
+            if (l < nc) st[comp * 33 + l] = soa[comp * kp.cs + kp.S + c0 + l];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < nc * NC; e += blockDim.x) {
+            const int l = e / NC, comp = e - l * NC;
+            aos[c0 * NC + e] = st[comp * 33 + l];
+        }
+        __syncthreads();
+    }
+}
+
+// L = R * (1/M_nn) in place (solver.hpp:42-54, mass_diag dg.hpp:42-50)
+__global__ void inverse_mass_kernel(KParams kp, double* q, int NC) {
+    const long ncell = (long)kp.S * kp.nzl;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < ncell * NC;
+         e += (long)gridDim.x * blockDim.x) {
+        const long c = e % ncell;
+        const int comp = (int)(e / ncell);
+        const int n = comp / 5;
+        const int i = (int)(c % kp.nx), j = (int)((c / kp.nx) % kp.ny), k = (int)(c / kp.S);
+        const double m = kp.dx[i] * kp.dy[j] * kp.dz[k + 1] / kp.tab[kp.off_massf + n];
+        const double inv = 1.0 / m;
+        double* p = q + comp * kp.cs + kp.S + c;
+        *p = *p * inv;
+    }
+}
+
+// ---------------------------------------------------------------- dt kernel
+// compute_dt (integrator.hpp:27-45): min over owned cells of cfl h / (|U|+|V|+
+// |W|+c) and the viscous bound. Positive doubles order like their bit
+// patterns, so the min is an integer atomicMin (order independent, exact).
+__global__ void dt_kernel(KParams kp, const double* __restrict__ q, double cfl, int degree,
+                          unsigned long long* dt_bits) {
+    const long n_owned = (long)kp.S * kp.nzl;
+    double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < n_owned;
+         c += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(c % kp.nx);
+        const int j = (int)((c / kp.nx) % kp.ny);
+        const int k = (int)(c / kp.S);
+        const long g = c + kp.S;  // skip the ghost layer
+        double avg[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) avg[v] = __ldg(q + v * kp.cs + g);
+        Prim w;
+        double bad = 0.0;
+        const int rc = prim_from_q(avg, kp.gas, w, bad);
+        if (rc) {
+            const long item = (long)i + (long)kp.nx * (j + (long)kp.ny * (k + kp.kglob0));
+            report_error(kp, err_key(0, 0, item, 0, 0, rc), bad);
+            continue;
+        }
+        const double h = fmin(fmin(__ldg(kp.dx + i), __ldg(kp.dy + j)), __ldg(kp.dz + k + 1));
+        const double p = 0.5 * w.rho / w.lam;
+        const double cs = sqrt(kp.gas.gamma * p / w.rho);
+        const double speed = fabs(w.U) + fabs(w.V) + fabs(w.W) + cs;
+        const double cand = cfl * h / speed;
+        if (cand < best) best = cand;
+        if (kp.gas.mu > 0.0) {
+            const double vis = cfl * h * h * w.rho / (2.0 * kp.gas.mu * (2.0 * degree + 1.0));
+            if (vis < best) best = vis;
+        }
+    }
+    // warp min then one atomic per warp (NaN never wins: comparisons are false)
+    unsigned long long bits = (unsigned long long)__double_as_longlong(best);
+    if (!(best >= 0.0)) bits = 0x7ff0000000000000ULL;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
+        bits = other < bits ? other : bits;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMin(dt_bits, bits);
+}
+
+// periodic single slab: ghost layer -1 <- layer nzl-1, ghost nzl <- layer 0
+__global__ void ghost_wrap_kernel(KParams kp, double* q, int ncomp) {
+    const long per = (long)kp.S;
+    const long total = per * ncomp * 2;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const long c = e % per;
+        const long r = e / per;
+        const int comp = (int)(r >> 1);
+        const int top = (int)(r & 1);
+        double* base = q + comp * kp.cs;
+        if (top)
+            base[(long)(kp.nzl + 1) * per + c] = base[per + c];
+        else
+            base[c] = base[(long)kp.nzl * per + c];
+    }
+}
+
+enum : int { CASE_ADV2D = 0, CASE_ADV3D = 1, CASE_VORTEX2D = 2, CASE_TGV = 3 };
+
+struct CaseParams {
+    int cid, dim;
+    double gamma, mach0, eps, t;
+    int npts;
+};
+
+// initial / exact fields (cases.hpp:78-124)
+__device__ __forceinline__ void case_field(const CaseParams& c, const double* x, double* q) {
+    const double pi = 3.14159265358979323846;
+    if (c.cid == CASE_ADV2D || c.cid == CASE_ADV3D) {
+        double s = x[0] + x[1] - 2.0 * c.t;
+        if (c.cid == CASE_ADV3D) s = x[0] + x[1] + x[2] - 3.0 * c.t;
+        const double rho = 1.0 + 0.2 * sin(pi * s);
+        const double W = c.cid == CASE_ADV3D ? 1.0 : 0.0;
+        const double E = 1.0 / (c.gamma - 1.0) + 0.5 * rho * (1.0 + 1.0 + W * W);
+        q[0] = rho;
+        q[1] = rho;
+        q[2] = rho;
+        q[3] = rho * W;
+        q[4] = E;
+    } else if (c.cid == CASE_VORTEX2D) {
+        auto wrap = [](double v) {
+            v = fmod(v, 10.0);
+            if (v < -5.0) v += 10.0;
+            if (v >= 5.0) v -= 10.0;
+            return v;
+        };
+        const double dx = wrap(x[0] - 5.0 - c.t), dy = wrap(x[1] - 5.0 - c.t);
+        const double r2 = dx * dx + dy * dy;
+        const double g = c.eps / (2.0 * pi) * exp(0.5 * (1.0 - r2));
+        const double U = 1.0 - g * dy, V = 1.0 + g * dx;
+        const double T = 1.0 - (c.gamma - 1.0) * c.eps * c.eps / (8.0 * c.gamma * pi * pi) * exp(1.0 - r2);
+        const double rho = pow(T, 1.0 / (c.gamma - 1.0));
+        const double p = rho * T;
+        q[0] = rho;
+        q[1] = rho * U;
+        q[2] = rho * V;
+        q[3] = 0.0;
+        q[4] = p / (c.gamma - 1.0) + 0.5 * rho * (U * U + V * V);
+    } else {
+        const double p0 = 1.0 / (c.gamma * c.mach0 * c.mach0);
+        const double U = sin(x[0]) * cos(x[1]) * cos(x[2]);
+        const double V = -cos(x[0]) * sin(x[1]) * cos(x[2]);
+        const double p = p0 + (cos(2.0 * x[0]) + cos(2.0 * x[1])) * (cos(2.0 * x[2]) + 2.0) / 16.0;
+        const double rho = p / p0;
+        q[0] = rho;
+        q[1] = rho * U;
+        q[2] = rho * V;
+        q[3] = 0.0;
+        q[4] = p / (c.gamma - 1.0) + 0.5 * rho * (U * U + V * V);
+    }
+}
+
+// project (dg.hpp:193-220): one thread per owned cell, (k+2)^3 points
+template <int NC>
+__global__ void __launch_bounds__(128) project_kernel(KParams kp, CaseParams cp,
+                                                      const double* __restrict__ ctr,
+                                                      double* __restrict__ q, long ncell) {
+    constexpr int N = NC / 5;
+    const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    const int i = (int)(c % kp.nx), j = (int)((c / kp.nx) % kp.ny), k = (int)(c / kp.S);
+    const double h[3] = {kp.dx[i], kp.dy[j], kp.dz[k + 1]};
+    const double x0[3] = {ctr[i], ctr[kp.nx + j], ctr[kp.nx + kp.ny + k]};
+    double acc[NC];
+#pragma unroll
+    for (int m = 0; m < NC; ++m) acc[m] = 0.0;
+    for (int p = 0; p < cp.npts; ++p) {
+        const double* r = kp.tab + kp.off_pref + 3 * p;
+        const double x[3] = {x0[0] + 0.5 * h[0] * r[0], x0[1] + 0.5 * h[1] * r[1], x0[2] + 0.5 * h[2] * r[2]};
+        double f[5];
+        case_field(cp, x, f);
+        const double wq = kp.tab[kp.off_pw + p];
+        const double* B = kp.tab + kp.off_pB + p * N;
+#pragma unroll
+        for (int n = 0; n < N; ++n) {
+            const double wb = wq * B[n];
+#pragma unroll
+            for (int v = 0; v < 5; ++v) acc[n * 5 + v] += wb * f[v];
+        }
+    }
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+        const double bn = kp.tab[kp.off_massf + n] / 8.0;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) q[(n * 5 + v) * kp.cs + kp.S + c] = acc[n * 5 + v] * bn;
+    }
+}
+
+// tgv_diagnostics partial sums (cases.hpp:165-204): per block
+// {sum vjac*ek, sum vjac*ens, sum vol}, fixed-order tree inside the block
+template <int NC>
+__global__ void __launch_bounds__(256) tgv_kernel(KParams kp, int npts,
+                                                  const double* __restrict__ q, long ncell,
+                                                  double* __restrict__ part) {
+    constexpr int N = NC / 5;
+    __shared__ double red[3][256];
+    double se = 0, sz = 0, sv = 0;
+    for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < ncell;
+         c += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(c % kp.nx), j = (int)((c / kp.nx) % kp.ny), k = (int)(c / kp.S);
+        const double h[3] = {kp.dx[i], kp.dy[j], kp.dz[k + 1]};
+        const double vjac = h[0] * h[1] * h[2] / 8.0;
+        double co[NC];
+#pragma unroll
+        for (int m = 0; m < NC; ++m) co[m] = q[m * kp.cs + kp.S + c];
+        double ek = 0, ens = 0;
+        for (int p = 0; p < npts; ++p) {
+            const double* B = kp.tab + kp.off_pB + p * N;
+            const double* dB = kp.tab + kp.off_pdB + p * 3 * N;
+            double e[20];
+#pragma unroll
+            for (int m = 0; m < 20; ++m) e[m] = 0.0;
+#pragma unroll
+            for (int n = 0; n < N; ++n) {
+#pragma unroll
+                for (int v = 0; v < 5; ++v) {
+                    const double cv = co[n * 5 + v];
+                    e[v] += B[n] * cv;
+                    e[5 + v] += dB[n] * cv;
+                    e[10 + v] += dB[N + n] * cv;
+                    e[15 + v] += dB[2 * N + n] * cv;
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < 5; ++v) {
+                e[5 + v] *= 2.0 / h[0];
+                e[10 + v] *= 2.0 / h[1];
+                e[15 + v] *= 2.0 / h[2];
+            }
+            const double inv = 1.0 / e[0];
+            const double U = e[1] * inv, V = e[2] * inv, W = e[3] * inv;
+            const double wq = kp.tab[kp.off_pw + p];
+            ek += wq * 0.5 * (e[1] * U + e[2] * V + e[3] * W);
+            const double vel[4] = {0.0, U, V, W};
+#define DVEL(comp, ax) ((e[5 + 5 * (ax) + (comp)] - vel[comp] * e[5 + 5 * (ax)]) * inv)
+            const double wx = DVEL(3, 1) - DVEL(2, 2);
+            const double wy = DVEL(1, 2) - DVEL(3, 0);
+            const double wz = DVEL(2, 0) - DVEL(1, 1);
+#undef DVEL
+            ens += wq * 0.5 * e[0] * (wx * wx + wy * wy + wz * wz);
+        }
+        se += vjac * ek;
+        sz += vjac * ens;
+        sv += h[0] * h[1] * h[2];
+    }
+    red[0][threadIdx.x] = se;
+    red[1][threadIdx.x] = sz;
+    red[2][threadIdx.x] = sv;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            for (int r = 0; r < 3; ++r) red[r][threadIdx.x] += red[r][threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int r = 0; r < 3; ++r) part[3 * blockIdx.x + r] = red[r][0];
+}
+
+inline void launch_project(int degree, int dim, const KParams& kp, const CaseParams& cp,
+                           const double* ctr, double* q, long ncell, cudaStream_t st) {
+    const int blocks = (int)((ncell + 127) / 128);
+    const int NC = 5 * (dim == 3 ? (degree == 1 ? 4 : degree == 2 ? 10 : 20) : (degree == 2 ? 6 : 10));
+    if (NC == 20) project_kernel<20><<<blocks, 128, 0, st>>>(kp, cp, ctr, q, ncell);
+    else if (NC == 30) project_kernel<30><<<blocks, 128, 0, st>>>(kp, cp, ctr, q, ncell);
+    else if (NC == 50) project_kernel<50><<<blocks, 128, 0, st>>>(kp, cp, ctr, q, ncell);
+    else project_kernel<100><<<blocks, 128, 0, st>>>(kp, cp, ctr, q, ncell);
+}
+
+inline void launch_tgv(int degree, int dim, const KParams& kp, int npts, const double* q, long ncell,
+                       double* part, int blocks, cudaStream_t st) {
+    const int NC = 5 * (dim == 3 ? (degree == 1 ? 4 : degree == 2 ? 10 : 20) : (degree == 2 ? 6 : 10));
+    if (NC == 20) tgv_kernel<20><<<blocks, 256, 0, st>>>(kp, npts, q, ncell, part);
+    else if (NC == 30) tgv_kernel<30><<<blocks, 256, 0, st>>>(kp, npts, q, ncell, part);
+    else if (NC == 50) tgv_kernel<50><<<blocks, 256, 0, st>>>(kp, npts, q, ncell, part);
+    else tgv_kernel<100><<<blocks, 256, 0, st>>>(kp, npts, q, ncell, part);
+}
+
+}  // namespace hgks_dev

@@ -1,0 +1,705 @@
+// C-ABI implementation of include/hgks_b200.h: the solver object, kernel
+// dispatch, host<->device layout transforms and the reference's error
+// semantics. There is no CPU path: every entry point that computes runs the
+// CUDA kernels of hgks_kernels.cuh and reports HGKS_ERR_CUDA if it cannot.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hgks_b200.h"
+#include "hgks_basis.h"
+#include "hgks_aux_kernels.cuh"
+#include "hgks_kernels.cuh"
+#include "hgks_launch.h"
+
+using namespace hgks_dev;
+
+namespace hgks_dev {
+bool pick_kernels(int degree, int dim, bool visc, KernelSet& ks, cudaError_t& err) {
+    if (degree == 2 && dim == 3) return pick_2_3(visc, ks, err);
+    if (degree == 3 && dim == 3) return pick_3_3(visc, ks, err);
+    if (degree == 1 && dim == 3) return pick_1_3(visc, ks, err);
+    if (degree == 2 && dim == 2) return pick_2_2(visc, ks, err);
+    if (degree == 3 && dim == 2) return pick_3_2(visc, ks, err);
+    return false;
+}
+}  // namespace hgks_dev
+
+struct hgks_solver {
+    hgks_config cfg{};
+    std::vector<double> xs, ys, zs;
+    hgks_host::Tables tabs;
+    KernelSet ks{};
+    int N = 0, NC = 0;
+    int nx = 0, ny = 0, nzl = 0, nz = 0, z0 = 0;
+    bool single = true;
+    long S = 0, cs = 0, fs = 0;
+    int zface_layers = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    // device memory
+    double *d_tab = nullptr, *d_dx = nullptr, *d_dy = nullptr, *d_dz = nullptr;
+    double *qa = nullptr, *qb = nullptr, *qs = nullptr, *L1 = nullptr, *Lt1 = nullptr;
+    double *R = nullptr, *Rt = nullptr, *tmp = nullptr;
+    double* face[3] = {nullptr, nullptr, nullptr};
+    unsigned long long* d_key = nullptr;  // [0] error key, [1] dt bits, [2] flux count
+    double* d_val = nullptr;
+    double* d_red = nullptr;  // reduction scratch
+    double time = 0.0;
+    // hooks
+    hgks_halo_fn halo = nullptr;
+    void* halo_user = nullptr;
+    hgks_min_fn dtmin = nullptr;
+    void* dtmin_user = nullptr;
+    const double* halo_array = nullptr;  // array whose ghosts the next exchange fills
+    bool count_fluxes = false;
+    long flux_evals = 0;
+    long launches = 0;
+    bool timing = false;
+    cudaEvent_t ev[6] = {};
+    double t_face = 0, t_cell = 0, t_other = 0;
+    // last error
+    std::string msg;
+    int e_code = 0, e_phase = -1;
+    long e_item = -1;
+    double e_value = 0.0;
+};
+
+namespace {
+
+int fail(hgks_solver* s, int code, const std::string& m) {
+    if (s) {
+        s->msg = m;
+        s->e_code = code;
+    }
+    return code;
+}
+
+int cuda_fail(hgks_solver* s, cudaError_t e, const char* where) {
+    return fail(s, HGKS_ERR_CUDA, std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                                   \
+    do {                                                           \
+        cudaError_t _e = (call);                                   \
+        if (_e != cudaSuccess) return cuda_fail(s, _e, #call);     \
+    } while (0)
+
+KParams make_params(hgks_solver* s, double dt, int stage) {
+    KParams kp{};
+    kp.nx = s->nx;
+    kp.ny = s->ny;
+    kp.nzl = s->nzl;
+    kp.S = (int)s->S;
+    kp.cs = s->cs;
+    kp.fs = s->fs;
+    kp.zface_layers = s->zface_layers;
+    kp.z_wrap = s->single ? 1 : 0;
+    kp.ncells_glob = (long)s->nx * s->ny * s->nz;
+    kp.kglob0 = s->z0;
+    kp.stage = stage;
+    kp.count_fluxes = s->count_fluxes ? 1 : 0;
+    kp.report = 0;
+    kp.dt = dt;
+    kp.gas.gamma = s->cfg.gamma;
+    kp.gas.gm1 = s->cfg.gamma - 1.0;
+    kp.gas.K = (5.0 - 3.0 * s->cfg.gamma) / (s->cfg.gamma - 1.0);
+    kp.gas.D = kp.gas.K + 3.0;
+    kp.gas.mu = s->cfg.mu;
+    kp.dx = s->d_dx;
+    kp.dy = s->d_dy;
+    kp.dz = s->d_dz;
+    kp.tab = s->d_tab;
+    const auto& t = s->tabs;
+    for (int a = 0; a < 3; ++a) {
+        for (int q = 0; q < 2; ++q) {
+            kp.off_fB[a][q] = t.off_fB[a][q];
+            kp.off_fdB[a][q] = t.off_fdB[a][q];
+        }
+        kp.off_fw[a] = t.off_fw[a];
+    }
+    kp.off_vB = t.off_vB;
+    kp.off_vdB = t.off_vdB;
+    kp.off_vw = t.off_vw;
+    kp.off_pB = t.off_pB;
+    kp.off_pdB = t.off_pdB;
+    kp.off_pw = t.off_pw;
+    kp.off_pref = t.off_pref;
+    kp.off_massf = t.off_massf;
+    kp.err_key = s->d_key;
+    kp.err_val = s->d_val;
+    kp.flux_count = s->d_key + 2;
+    return kp;
+}
+
+std::string fmt_f(double v) {  // std::to_string(double) == "%f"
+    char b[64];
+    std::snprintf(b, sizeof b, "%f", v);
+    return b;
+}
+
+// fill ghost layers of array a before a residual: periodic wrap for a single
+// slab, the user's halo exchange otherwise
+int fill_ghosts(hgks_solver* s, double* a) {
+    if (s->single) {
+        KParams kp = make_params(s, 0.0, 0);
+        const long total = s->S * s->NC * 2;
+        const int blocks = (int)std::min<long>((total + 255) / 256, 148L * 16);
+        ghost_wrap_kernel<<<blocks, 256, 0, s->stream>>>(kp, a, s->NC);
+        ++s->launches;
+        CK(cudaGetLastError());
+        return HGKS_OK;
+    }
+    if (!s->halo) return fail(s, HGKS_ERR_CONFIG, "multi-slab solver has no halo exchange set");
+    s->halo_array = a;
+    const int rc = s->halo(s->halo_user, s);
+    if (rc != 0) return fail(s, HGKS_ERR_CUDA, "halo exchange callback failed");
+    return HGKS_OK;
+}
+
+int reset_error(hgks_solver* s) {
+    const unsigned long long init[2] = {~0ull, ~0ull};
+    CK(cudaMemcpyAsync(s->d_key, init, sizeof init, cudaMemcpyHostToDevice, s->stream));
+    return HGKS_OK;
+}
+
+// Decode the winning error key; re-run the failing tile in report mode to get
+// the offending value; shape the message as the reference does.
+int finish_error(hgks_solver* s, unsigned long long key, const double* stage_inputs[2],
+                 double dt) {
+    const int stage = (int)(key >> 62) & 1;
+    const int phase = (int)(key >> 61) & 1;
+    const long item = (long)((key >> 22) & ((1ull << 39) - 1));
+    const int code = (int)(key & 0xff);
+    KParams kp = make_params(s, dt, stage);
+    kp.report = 1;
+    kp.count_fluxes = 0;
+    int tile[4];
+    const long nc = (long)s->nx * s->ny * s->nz;
+    long cell = phase == 0 ? item % nc : item;
+    const int axis = phase == 0 ? (int)(item / nc) : 0;
+    const int i = (int)(cell % s->nx), j = (int)((cell / s->nx) % s->ny);
+    const int k = (int)(cell / ((long)s->nx * s->ny)) - s->z0;
+    double* nof[3] = {s->face[0], s->face[1], s->face[2]};
+    const double* in = stage_inputs[stage];
+    if (phase == 0) {
+        tile[0] = i / 32;
+        tile[1] = j;
+        tile[2] = k;
+        tile[3] = axis;
+        s->ks.face(kp, in, nof, s->stream, 1, tile);
+    } else {
+        tile[0] = i / s->ks.cell_tc;
+        tile[1] = j;
+        tile[2] = k;
+        tile[3] = 0;
+        s->ks.cell(kp, MODE_RESIDUAL, in, nof, nullptr, nullptr, nullptr, nullptr, nullptr,
+                   nullptr, s->stream, 1, tile);
+    }
+    CK(cudaGetLastError());
+    double val = 0.0;
+    CK(cudaMemcpyAsync(&val, s->d_val, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    s->e_code = HGKS_ERR_STATE;
+    s->e_phase = phase;
+    s->e_item = item;
+    s->e_value = val;
+    const std::string inner = code == ERR_DENSITY ? "non-positive density: rho=" + fmt_f(val)
+                                                  : "non-positive pressure: p=" + fmt_f(val);
+    s->msg = "item " + std::to_string(item) + ": " + inner;
+    return HGKS_ERR_STATE;
+}
+
+void ev_record(hgks_solver* s, int i) {
+    if (s->timing) cudaEventRecord(s->ev[i], s->stream);
+}
+
+// One residual evaluation of `in` (ghosts filled here) in the given mode.
+int run_residual(hgks_solver* s, double* in, double dt, int stage, int mode, const double* qn,
+                 double* o0, double* o1, double* o2) {
+    int rc = fill_ghosts(s, in);
+    if (rc) return rc;
+    KParams kp = make_params(s, dt, stage);
+    ev_record(s, stage * 3 + 0);
+    s->ks.face(kp, in, s->face, s->stream, 0, nullptr);
+    s->launches += 3;
+    ev_record(s, stage * 3 + 1);
+    s->ks.cell(kp, mode, in, s->face, qn, s->L1, s->Lt1, o0, o1, o2, s->stream, 0, nullptr);
+    s->launches += 1;
+    ev_record(s, stage * 3 + 2);
+    CK(cudaGetLastError());
+    return HGKS_OK;
+}
+
+int check_error(hgks_solver* s, const double* stage_inputs[2], double dt, bool* failed) {
+    unsigned long long h[3];
+    CK(cudaMemcpyAsync(h, s->d_key, sizeof h, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    if (s->count_fluxes) {
+        s->flux_evals += (long)h[2];
+        const unsigned long long z = 0;
+        CK(cudaMemcpyAsync(s->d_key + 2, &z, sizeof z, cudaMemcpyHostToDevice, s->stream));
+    }
+    *failed = h[0] != ~0ull;
+    if (*failed) return finish_error(s, h[0], stage_inputs, dt);
+    return HGKS_OK;
+}
+
+void collect_times(hgks_solver* s, int stages) {
+    if (!s->timing) return;
+    cudaEventSynchronize(s->ev[stages * 3 - 1]);
+    float a = 0, b = 0;
+    s->t_face = s->t_cell = 0;
+    for (int st = 0; st < stages; ++st) {
+        cudaEventElapsedTime(&a, s->ev[st * 3 + 0], s->ev[st * 3 + 1]);
+        cudaEventElapsedTime(&b, s->ev[st * 3 + 1], s->ev[st * 3 + 2]);
+        s->t_face += a;
+        s->t_cell += b;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int hgks_abi_version(void) { return HGKS_ABI_VERSION; }
+
+int hgks_create(const hgks_config* cfg, hgks_solver** out) {
+    if (!cfg || !out) return HGKS_ERR_CONFIG;
+    *out = nullptr;
+    auto* s = new hgks_solver();
+    s->cfg = *cfg;
+    auto bad = [&](const char* m) {
+        s->msg = m;
+        *out = s;  // returned so the caller can read the message, then destroy
+        s->e_code = HGKS_ERR_CONFIG;
+        return HGKS_ERR_CONFIG;
+    };
+    if (cfg->nx < 1 || cfg->ny < 1 || cfg->nz < 1) return bad("mesh: need at least one cell per axis");
+    if (!cfg->xs || !cfg->ys || !cfg->zs) return bad("mesh: node arrays required");
+    if (cfg->degree < 1 || cfg->degree > 3) return bad("build_basis: degree must be 2 or 3 (1 = P1 extension)");
+    if (cfg->dim != 2 && cfg->dim != 3) return bad("build_basis: dim must be 2 or 3");
+    if (cfg->dim == 2 && cfg->degree == 1) return bad("P1 is supported in 3-D only");
+    if (cfg->dim == 2 && cfg->nz != 1) return bad("2-D mode runs on one z cell");
+    if (!(cfg->gamma > 1.0) || (5.0 - 3.0 * cfg->gamma) < 0.0)
+        return bad("GasModel: gamma gives negative internal dof");
+    if (cfg->mu < 0.0) return bad("GasModel: negative viscosity");
+    s->xs.assign(cfg->xs, cfg->xs + cfg->nx + 1);
+    s->ys.assign(cfg->ys, cfg->ys + cfg->ny + 1);
+    s->zs.assign(cfg->zs, cfg->zs + cfg->nz + 1);
+    for (const auto* v : {&s->xs, &s->ys, &s->zs})
+        for (size_t i = 1; i < v->size(); ++i)
+            if (!((*v)[i] > (*v)[i - 1])) return bad("Mesh: node coordinates must be strictly increasing");
+    s->nx = cfg->nx;
+    s->ny = cfg->ny;
+    s->nz = cfg->nz;
+    s->z0 = cfg->z_count > 0 ? cfg->z_begin : 0;
+    s->nzl = cfg->z_count > 0 ? cfg->z_count : cfg->nz;
+    if (s->z0 < 0 || s->z0 + s->nzl > s->nz) return bad("slab: z range outside the mesh");
+    s->single = s->nzl == s->nz;
+    s->tabs = hgks_host::make_tables(cfg->degree, cfg->dim);
+    s->N = s->tabs.basis.N;
+    s->NC = s->N * 5;
+    s->S = (long)s->nx * s->ny;
+    const long pad = 64;
+    s->cs = ((s->S * (s->nzl + 2) + pad - 1) / pad) * pad;
+    s->zface_layers = s->single ? s->nzl : s->nzl + 1;
+    s->fs = ((s->S * s->zface_layers + pad - 1) / pad) * pad;
+    cudaError_t ce;
+    if (!pick_kernels(cfg->degree, cfg->dim, cfg->mu > 0.0, s->ks, ce)) return bad("no kernels for this degree/dim");
+    *out = s;
+    CK(cudaSetDevice(cfg->device));
+    if (ce != cudaSuccess) return cuda_fail(s, ce, "cudaFuncSetAttribute");
+    CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    s->own_stream = true;
+    for (auto& e : s->ev) CK(cudaEventCreate(&e));
+    const size_t arr = (size_t)s->NC * s->cs * sizeof(double);
+    CK(cudaMalloc(&s->d_tab, s->tabs.img.size() * sizeof(double)));
+    CK(cudaMemcpy(s->d_tab, s->tabs.img.data(), s->tabs.img.size() * sizeof(double), cudaMemcpyHostToDevice));
+    std::vector<double> dx(s->nx), dy(s->ny), dz(s->nzl + 2);
+    for (int i = 0; i < s->nx; ++i) dx[i] = s->xs[i + 1] - s->xs[i];
+    for (int j = 0; j < s->ny; ++j) dy[j] = s->ys[j + 1] - s->ys[j];
+    for (int k = -1; k <= s->nzl; ++k) {
+        const int kg = ((s->z0 + k) % s->nz + s->nz) % s->nz;
+        dz[k + 1] = s->zs[kg + 1] - s->zs[kg];
+    }
+    CK(cudaMalloc(&s->d_dx, dx.size() * sizeof(double)));
+    CK(cudaMalloc(&s->d_dy, dy.size() * sizeof(double)));
+    CK(cudaMalloc(&s->d_dz, dz.size() * sizeof(double)));
+    CK(cudaMemcpy(s->d_dx, dx.data(), dx.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(s->d_dy, dy.data(), dy.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(s->d_dz, dz.data(), dz.size() * sizeof(double), cudaMemcpyHostToDevice));
+    for (double** p : {&s->qa, &s->qb, &s->qs, &s->L1, &s->Lt1}) {
+        CK(cudaMalloc(p, arr));
+        CK(cudaMemset(*p, 0, arr));
+    }
+    for (int a = 0; a < 3; ++a) {
+        const size_t fb = (size_t)s->ks.nfp[a] * 10 * s->fs * sizeof(double);
+        CK(cudaMalloc(&s->face[a], fb));
+        CK(cudaMemset(s->face[a], 0, fb));
+    }
+    CK(cudaMalloc(&s->d_key, 4 * sizeof(unsigned long long)));
+    CK(cudaMemset(s->d_key, 0, 4 * sizeof(unsigned long long)));
+    CK(cudaMalloc(&s->d_val, 4 * sizeof(double)));
+    CK(cudaMalloc(&s->d_red, 4096 * sizeof(double)));
+    return HGKS_OK;
+}
+
+void hgks_destroy(hgks_solver* s) {
+    if (!s) return;
+    for (double* p : {s->d_tab, s->d_dx, s->d_dy, s->d_dz, s->qa, s->qb, s->qs, s->L1, s->Lt1,
+                      s->R, s->Rt, s->tmp, s->face[0], s->face[1], s->face[2], s->d_val, s->d_red})
+        if (p) cudaFree(p);
+    if (s->d_key) cudaFree(s->d_key);
+    for (auto& e : s->ev)
+        if (e) cudaEventDestroy(e);
+    if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+}
+
+const char* hgks_last_error(const hgks_solver* s) { return s ? s->msg.c_str() : "null solver"; }
+
+void hgks_error_info(const hgks_solver* s, int* code, int* phase, long* item, double* value) {
+    if (code) *code = s->e_code;
+    if (phase) *phase = s->e_phase;
+    if (item) *item = s->e_item;
+    if (value) *value = s->e_value;
+}
+
+int hgks_num_basis(const hgks_solver* s) { return s->N; }
+long hgks_num_coeffs(const hgks_solver* s) { return s->S * s->nzl * s->NC; }
+int hgks_face_points(const hgks_solver* s, int axis) { return s->ks.nfp[axis]; }
+
+}  // extern "C"
+
+namespace {
+
+int ensure_tmp(hgks_solver* s) {
+    if (!s->tmp) CK(cudaMalloc(&s->tmp, (size_t)s->NC * s->cs * sizeof(double)));
+    return HGKS_OK;
+}
+
+// host AoS (owned cells) -> device SoA array (ghost layers untouched)
+int upload_aos(hgks_solver* s, const double* host, double* dst) {
+    int rc = ensure_tmp(s);
+    if (rc) return rc;
+    const size_t n = (size_t)hgks_num_coeffs(s);
+    CK(cudaMemcpyAsync(s->tmp, host, n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    KParams kp = make_params(s, 0.0, 0);
+    aos_to_soa_kernel<<<(int)std::min<long>(((long)n + 255) / 256, 148L * 32), 256, 0, s->stream>>>(
+        kp, s->tmp, dst, s->NC);
+    ++s->launches;
+    CK(cudaGetLastError());
+    return HGKS_OK;
+}
+
+int download_aos(hgks_solver* s, const double* src, double* host) {
+    int rc = ensure_tmp(s);
+    if (rc) return rc;
+    const size_t n = (size_t)hgks_num_coeffs(s);
+    KParams kp = make_params(s, 0.0, 0);
+    soa_to_aos_kernel<<<(int)std::min<long>(((long)n + 255) / 256, 148L * 32), 256, 0, s->stream>>>(
+        kp, src, s->tmp, s->NC);
+    ++s->launches;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(host, s->tmp, n * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return HGKS_OK;
+}
+
+// face buffers -> reference ws.face layout [f*(npts*10) + p*10 + c]
+int download_faces(hgks_solver* s, int axis, double* host) {
+    const int nfp = s->ks.nfp[axis];
+    const long nf = s->S * s->nzl;
+    std::vector<double> dev((size_t)nfp * 10 * s->fs);
+    CK(cudaMemcpyAsync(dev.data(), s->face[axis], dev.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    for (long f = 0; f < nf; ++f)
+        for (int r = 0; r < nfp * 10; ++r) host[f * nfp * 10 + r] = dev[(size_t)r * s->fs + f];
+    return HGKS_OK;
+}
+
+int do_step(hgks_solver* s, double dt) {
+    int rc = reset_error(s);
+    if (rc) return rc;
+    // stage 1: L1, Lt1, q* from q^n (qa)
+    rc = run_residual(s, s->qa, dt, 0, MODE_STAGE1, nullptr, s->qs, s->L1, s->Lt1);
+    if (rc) return rc;
+    // stage 2: q^{n+1} into qb from q*, q^n, L1, Lt1
+    rc = run_residual(s, s->qs, dt, 1, MODE_STAGE2, s->qa, s->qb, nullptr, nullptr);
+    if (rc) return rc;
+    const double* inputs[2] = {s->qa, s->qs};
+    bool failed = false;
+    rc = check_error(s, inputs, dt, &failed);
+    if (rc) return rc;
+    collect_times(s, 2);
+    std::swap(s->qa, s->qb);
+    s->time += dt;
+    return HGKS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hgks_set_state(hgks_solver* s, const double* coeffs, double time) {
+    const int rc = upload_aos(s, coeffs, s->qa);
+    if (rc) return rc;
+    s->time = time;
+    CK(cudaStreamSynchronize(s->stream));
+    return HGKS_OK;
+}
+
+int hgks_get_state(hgks_solver* s, double* coeffs, double* time) {
+    if (time) *time = s->time;
+    return coeffs ? download_aos(s, s->qa, coeffs) : HGKS_OK;
+}
+
+int hgks_residual(hgks_solver* s, const double* coeffs, double dt, double* R, double* Rt,
+                  double* face0, double* face1, double* face2) {
+    const size_t arr = (size_t)s->NC * s->cs * sizeof(double);
+    if (!s->R) CK(cudaMalloc(&s->R, arr));
+    if (!s->Rt) CK(cudaMalloc(&s->Rt, arr));
+    double* in = s->qa;
+    int rc;
+    if (coeffs) {
+        rc = upload_aos(s, coeffs, s->qs);
+        if (rc) return rc;
+        in = s->qs;
+    }
+    rc = reset_error(s);
+    if (rc) return rc;
+    rc = run_residual(s, in, dt, 0, MODE_RESIDUAL, nullptr, s->R, s->Rt, nullptr);
+    if (rc) return rc;
+    const double* inputs[2] = {in, in};
+    bool failed = false;
+    rc = check_error(s, inputs, dt, &failed);
+    if (rc) return rc;
+    collect_times(s, 1);
+    if (R && (rc = download_aos(s, s->R, R))) return rc;
+    if (Rt && (rc = download_aos(s, s->Rt, Rt))) return rc;
+    double* fh[3] = {face0, face1, face2};
+    for (int a = 0; a < 3; ++a)
+        if (fh[a] && (rc = download_faces(s, a, fh[a]))) return rc;
+    return HGKS_OK;
+}
+
+int hgks_apply_inverse_mass(hgks_solver* s, const double* R, double* L) {
+    int rc = upload_aos(s, R, s->qs);
+    if (rc) return rc;
+    KParams kp = make_params(s, 0.0, 0);
+    const long n = hgks_num_coeffs(s);
+    inverse_mass_kernel<<<(int)std::min<long>((n + 255) / 256, 148L * 32), 256, 0, s->stream>>>(
+        kp, s->qs, s->NC);
+    ++s->launches;
+    CK(cudaGetLastError());
+    return download_aos(s, s->qs, L);
+}
+
+int hgks_compute_dt(hgks_solver* s, double cfl, double* dt) {
+    int rc = reset_error(s);
+    if (rc) return rc;
+    KParams kp = make_params(s, 0.0, 0);
+    dt_kernel<<<148 * 4, 256, 0, s->stream>>>(kp, s->qa, cfl, s->cfg.degree, s->d_key + 1);
+    ++s->launches;
+    CK(cudaGetLastError());
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, s->d_key, sizeof h, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    if (h[0] != ~0ull) {
+        // compute_dt throws the bare state error, not wrapped in worker_error
+        const long item = (long)((h[0] >> 22) & ((1ull << 39) - 1));
+        const int code = (int)(h[0] & 0xff);
+        kp.report = 1;
+        dt_kernel<<<148 * 4, 256, 0, s->stream>>>(kp, s->qa, cfl, s->cfg.degree, s->d_key + 3);
+        double val = 0;
+        CK(cudaMemcpyAsync(&val, s->d_val, sizeof val, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        s->e_code = HGKS_ERR_STATE;
+        s->e_phase = 2;
+        s->e_item = item;
+        s->e_value = val;
+        s->msg = code == ERR_DENSITY ? "non-positive density: rho=" + fmt_f(val)
+                                     : "non-positive pressure: p=" + fmt_f(val);
+        return HGKS_ERR_STATE;
+    }
+    double v;
+    std::memcpy(&v, &h[1], sizeof v);
+    if (s->dtmin) {
+        if (s->dtmin(s->dtmin_user, &v) != 0) return fail(s, HGKS_ERR_CUDA, "dt reduction callback failed");
+    }
+    if (!(v > 0.0) || !std::isfinite(v)) return fail(s, HGKS_ERR_DT, "compute_dt: nonpositive dt");
+    *dt = v;
+    return HGKS_OK;
+}
+
+int hgks_step(hgks_solver* s, double dt) { return do_step(s, dt); }
+
+int hgks_two_stage_step_host(hgks_solver* s, double* q, double dt) {
+    int rc = upload_aos(s, q, s->qa);
+    if (rc) return rc;
+    rc = do_step(s, dt);
+    if (rc) return rc;
+    return download_aos(s, s->qa, q);
+}
+
+int hgks_advance(hgks_solver* s, double t_end, double cfl, double dt_fixed, double record_interval,
+                 int* steps) {
+    double t = s->time;
+    double next_record = record_interval > 0 ? (std::floor(t / record_interval + 1e-9) + 1) * record_interval : 0;
+    int n = 0;
+    while (t < t_end - 1e-14 * t_end) {
+        double dt = dt_fixed;
+        if (!(dt_fixed > 0.0)) {
+            const int rc = hgks_compute_dt(s, cfl, &dt);
+            if (rc) {
+                if (steps) *steps = n;
+                return rc;
+            }
+        }
+        dt = std::min(dt, t_end - t);
+        if (record_interval > 0) dt = std::min(dt, next_record - t);
+        const int rc = do_step(s, dt);
+        if (rc) {
+            if (rc == HGKS_ERR_STATE) s->msg += " at t=" + std::to_string(t);
+            if (steps) *steps = n;
+            return rc;
+        }
+        t += dt;
+        s->time = t;
+        ++n;
+        if (record_interval > 0 && t >= next_record - 1e-12) next_record += record_interval;
+    }
+    if (steps) *steps = n;
+    return HGKS_OK;
+}
+
+void hgks_set_count_fluxes(hgks_solver* s, int on) {
+    s->count_fluxes = on != 0;
+    s->flux_evals = 0;
+}
+long hgks_flux_evaluations(const hgks_solver* s) { return s->flux_evals; }
+
+int hgks_project_case(hgks_solver* s, const char* case_name, double t) {
+    int cid;
+    if (!std::strcmp(case_name, "adv2d")) cid = CASE_ADV2D;
+    else if (!std::strcmp(case_name, "adv3d")) cid = CASE_ADV3D;
+    else if (!std::strcmp(case_name, "vortex2d")) cid = CASE_VORTEX2D;
+    else if (!std::strcmp(case_name, "tgv")) cid = CASE_TGV;
+    else return fail(s, HGKS_ERR_CONFIG, std::string("unknown case: ") + case_name);
+    KParams kp = make_params(s, 0.0, 0);
+    std::vector<double> hx(s->nx), hy(s->ny), hz(s->nzl);
+    for (int i = 0; i < s->nx; ++i) hx[i] = 0.5 * (s->xs[i] + s->xs[i + 1]);
+    for (int j = 0; j < s->ny; ++j) hy[j] = 0.5 * (s->ys[j] + s->ys[j + 1]);
+    for (int k = 0; k < s->nzl; ++k) hz[k] = 0.5 * (s->zs[s->z0 + k] + s->zs[s->z0 + k + 1]);
+    std::vector<double> ctr;
+    ctr.insert(ctr.end(), hx.begin(), hx.end());
+    ctr.insert(ctr.end(), hy.begin(), hy.end());
+    ctr.insert(ctr.end(), hz.begin(), hz.end());
+    double* d_ctr = nullptr;
+    CK(cudaMalloc(&d_ctr, ctr.size() * sizeof(double)));
+    CK(cudaMemcpyAsync(d_ctr, ctr.data(), ctr.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    CaseParams cp;
+    cp.cid = cid;
+    cp.dim = s->cfg.dim;
+    cp.gamma = s->cfg.gamma;
+    cp.mach0 = 0.1;
+    cp.eps = 5.0;
+    cp.t = t;
+    cp.npts = s->tabs.proj.npts;
+    const long ncell = s->S * s->nzl;
+    launch_project(s->cfg.degree, s->cfg.dim, kp, cp, d_ctr, s->qa, ncell, s->stream);
+    ++s->launches;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s->stream));
+    cudaFree(d_ctr);
+    s->time = 0.0;
+    return HGKS_OK;
+}
+
+int hgks_tgv_diagnostics(hgks_solver* s, double* ek_vol, double* ens_vol, double* volume) {
+    KParams kp = make_params(s, 0.0, 0);
+    const long ncell = s->S * s->nzl;
+    const int blocks = 148 * 2;
+    launch_tgv(s->cfg.degree, s->cfg.dim, kp, s->tabs.proj.npts, s->qa, ncell, s->d_red, blocks, s->stream);
+    ++s->launches;
+    CK(cudaGetLastError());
+    std::vector<double> part(3 * blocks);
+    CK(cudaMemcpyAsync(part.data(), s->d_red, part.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    double e = 0, z = 0, v = 0;
+    for (int b = 0; b < blocks; ++b) {  // fixed order
+        e += part[3 * b];
+        z += part[3 * b + 1];
+        v += part[3 * b + 2];
+    }
+    if (ek_vol) *ek_vol = e;
+    if (ens_vol) *ens_vol = z;
+    if (volume) *volume = v;
+    return HGKS_OK;
+}
+
+int hgks_halo_buffers(hgks_solver* s, unsigned long long* send_lo, unsigned long long* send_hi,
+                      unsigned long long* recv_lo, unsigned long long* recv_hi, long* layer_bytes,
+                      long* comp_stride_bytes, int* ncomp) {
+    const double* a = s->halo_array ? s->halo_array : s->qa;
+    const size_t L = (size_t)s->S;
+    if (send_lo) *send_lo = (unsigned long long)(a + L);
+    if (send_hi) *send_hi = (unsigned long long)(a + (size_t)s->nzl * L);
+    if (recv_lo) *recv_lo = (unsigned long long)(a);
+    if (recv_hi) *recv_hi = (unsigned long long)(a + (size_t)(s->nzl + 1) * L);
+    if (layer_bytes) *layer_bytes = (long)(L * sizeof(double));
+    if (comp_stride_bytes) *comp_stride_bytes = (long)(s->cs * sizeof(double));
+    if (ncomp) *ncomp = s->NC;
+    return HGKS_OK;
+}
+
+void hgks_set_halo_exchange(hgks_solver* s, hgks_halo_fn fn, void* user) {
+    s->halo = fn;
+    s->halo_user = user;
+}
+
+void hgks_set_dt_reduce(hgks_solver* s, hgks_min_fn fn, void* user) {
+    s->dtmin = fn;
+    s->dtmin_user = user;
+}
+
+int hgks_set_stream(hgks_solver* s, void* stream) {
+    if (s->own_stream && s->stream) {
+        CK(cudaStreamSynchronize(s->stream));
+        cudaStreamDestroy(s->stream);
+    }
+    if (stream) {
+        s->stream = (cudaStream_t)stream;
+        s->own_stream = false;
+    } else {
+        CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+        s->own_stream = true;
+    }
+    return HGKS_OK;
+}
+
+void* hgks_get_stream(hgks_solver* s) { return (void*)s->stream; }
+
+int hgks_synchronize(hgks_solver* s) {
+    CK(cudaStreamSynchronize(s->stream));
+    return HGKS_OK;
+}
+
+long hgks_launch_count(const hgks_solver* s) { return s->launches; }
+
+void hgks_set_kernel_timing(hgks_solver* s, int on) { s->timing = on != 0; }
+
+int hgks_kernel_times(hgks_solver* s, double* face_ms, double* cell_ms, double* other_ms) {
+    if (face_ms) *face_ms = s->t_face;
+    if (cell_ms) *cell_ms = s->t_cell;
+    if (other_ms) *other_ms = s->t_other;
+    return HGKS_OK;
+}
+
+}  // extern "C"

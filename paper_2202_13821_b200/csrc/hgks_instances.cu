@@ -1,0 +1,108 @@
+// Explicit kernel instantiation unit: one translation unit per
+// (degree, dim) family (HGKS_INST_P, HGKS_INST_DIM), compiled in parallel by
+// build.py. Each exports pick_<P>_<DIM>() for the dispatcher in hgks_capi.cu.
+#include "hgks_launch.h"
+
+#ifndef HGKS_INST_P
+#define HGKS_INST_P 2
+#define HGKS_INST_DIM 3
+#endif
+
+namespace hgks_dev {
+namespace {
+
+template <int P, int DIM, bool VISC>
+struct Launch {
+    using SH = Shape<P, DIM>;
+    static int face_smem() { return 2 * SH::NC * 32 * (int)sizeof(double); }
+    static int cell_smem() { return (SH::NC * SH::TC + SH::NVP * 30 * SH::TC) * (int)sizeof(double); }
+
+    template <int AXIS>
+    static void face_axis(const KParams& kp, const double* q, double* f, cudaStream_t st,
+                          int report, const int* tile) {
+        constexpr int NFP = SH::template nfp<AXIS>();
+        const int layers = AXIS == 2 ? kp.zface_layers : kp.nzl;
+        dim3 grid((kp.nx + 31) / 32, kp.ny, layers);
+        int t[3] = {0, 0, 0};
+        if (report) {
+            grid = dim3(1, 1, 1);
+            t[0] = tile[0];
+            t[1] = tile[1];
+            t[2] = tile[2];
+        }
+        face_kernel<P, DIM, VISC, AXIS><<<grid, 32 * NFP, face_smem(), st>>>(kp, q, f, t[0], t[1], t[2]);
+    }
+    static void face(const KParams& kp, const double* q, double* const f[3], cudaStream_t st,
+                     int report, const int* tile) {
+        // report mode re-runs only the failing axis' tile (tile[3] = axis)
+        if (!report || tile[3] == 0) face_axis<0>(kp, q, f[0], st, report, tile);
+        if (!report || tile[3] == 1) face_axis<1>(kp, q, f[1], st, report, tile);
+        if (!report || tile[3] == 2) face_axis<2>(kp, q, f[2], st, report, tile);
+    }
+    static void cell(const KParams& kp, int mode, const double* qin, double* const f[3],
+                     const double* qn, const double* L1, const double* Lt1, double* o0, double* o1,
+                     double* o2, cudaStream_t st, int report, const int* tile) {
+        dim3 grid((kp.nx + SH::TC - 1) / SH::TC, kp.ny, kp.nzl);
+        int t[3] = {0, 0, 0};
+        if (report) {
+            grid = dim3(1, 1, 1);
+            t[0] = tile[0];
+            t[1] = tile[1];
+            t[2] = tile[2];
+        }
+        const int smem = cell_smem();
+        if (mode == MODE_RESIDUAL)
+            cell_kernel<P, DIM, VISC, MODE_RESIDUAL><<<grid, SH::NT_CELL, smem, st>>>(
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, t[0], t[1], t[2]);
+        else if (mode == MODE_STAGE1)
+            cell_kernel<P, DIM, VISC, MODE_STAGE1><<<grid, SH::NT_CELL, smem, st>>>(
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, t[0], t[1], t[2]);
+        else
+            cell_kernel<P, DIM, VISC, MODE_STAGE2><<<grid, SH::NT_CELL, smem, st>>>(
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, t[0], t[1], t[2]);
+    }
+    static cudaError_t configure() {
+        cudaError_t e = cudaSuccess;
+        auto set = [&](const void* fn, int bytes) {
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        };
+        set((const void*)face_kernel<P, DIM, VISC, 0>, face_smem());
+        set((const void*)face_kernel<P, DIM, VISC, 1>, face_smem());
+        set((const void*)face_kernel<P, DIM, VISC, 2>, face_smem());
+        set((const void*)cell_kernel<P, DIM, VISC, MODE_RESIDUAL>, cell_smem());
+        set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE1>, cell_smem());
+        set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE2>, cell_smem());
+        return e;
+    }
+    static KernelSet set() {
+        KernelSet k;
+        k.face = &face;
+        k.cell = &cell;
+        for (int a = 0; a < 3; ++a) k.face_smem[a] = face_smem();
+        k.cell_smem = cell_smem();
+        k.cell_tc = SH::TC;
+        k.nfp[0] = SH::template nfp<0>();
+        k.nfp[1] = SH::template nfp<1>();
+        k.nfp[2] = SH::template nfp<2>();
+        return k;
+    }
+};
+
+}  // namespace
+
+#define HGKS_CAT(a, b, c) a##_##b##_##c
+#define HGKS_PICKNAME(P, D) HGKS_CAT(pick, P, D)
+
+bool HGKS_PICKNAME(HGKS_INST_P, HGKS_INST_DIM)(bool visc, KernelSet& ks, cudaError_t& err) {
+    if (visc) {
+        err = Launch<HGKS_INST_P, HGKS_INST_DIM, true>::configure();
+        ks = Launch<HGKS_INST_P, HGKS_INST_DIM, true>::set();
+    } else {
+        err = Launch<HGKS_INST_P, HGKS_INST_DIM, false>::configure();
+        ks = Launch<HGKS_INST_P, HGKS_INST_DIM, false>::set();
+    }
+    return true;
+}
+
+}  // namespace hgks_dev

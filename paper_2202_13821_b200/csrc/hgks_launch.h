@@ -1,0 +1,34 @@
+// Kernel-set dispatch shared by the C-ABI and the per-(degree, dim)
+// instantiation units (hgks_instances.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "hgks_kernels.cuh"
+
+namespace hgks_dev {
+
+struct KernelSet {
+    void (*face)(const KParams&, const double* q, double* const f[3], cudaStream_t, int report,
+                 const int* tile);
+    void (*cell)(const KParams&, int mode, const double* qin, double* const f[3], const double* qn,
+                 const double* L1, const double* Lt1, double* o0, double* o1, double* o2,
+                 cudaStream_t, int report, const int* tile);
+    int face_smem[3];
+    int cell_smem;
+    int cell_tc;
+    int nfp[3];
+};
+
+// one per instantiated (degree, dim): configures shared memory and fills ks
+bool pick_kernels(int degree, int dim, bool visc, KernelSet& ks, cudaError_t& err);
+
+#define HGKS_DECLARE_PICK(P, D) \
+    bool pick_##P##_##D(bool visc, KernelSet& ks, cudaError_t& err);
+HGKS_DECLARE_PICK(1, 3)
+HGKS_DECLARE_PICK(2, 3)
+HGKS_DECLARE_PICK(3, 3)
+HGKS_DECLARE_PICK(2, 2)
+HGKS_DECLARE_PICK(3, 2)
+
+}  // namespace hgks_dev

@@ -1,0 +1,520 @@
+"""Host-side mirror of the reference solver interface (proj/include/hgks),
+driving the B200 kernels through the C ABI (include/hgks_b200.h).
+
+Names, argument meanings and error behaviour follow the reference:
+
+=====================================  =====================================
+reference (C++)                        here
+=====================================  =====================================
+GasModel::make (core.hpp:35)           GasModel.make
+Mesh::make (mesh.hpp:22)               Mesh.make
+Scheme::make (dg.hpp:274)              Scheme.make
+CaseConfig::named (cases.hpp:12)       CaseConfig.named
+build_mesh (cases.hpp:59)              build_mesh
+setup_run (solver.hpp:29)              setup_run
+residual (dg.hpp:354)                  Solver.residual / residual()
+apply_inverse_mass (solver.hpp:42)     Solver.apply_inverse_mass
+compute_dt (integrator.hpp:27)         Solver.compute_dt / compute_dt()
+two_stage_step (integrator.hpp:64)     Solver.step / two_stage_step()
+advance (solver.hpp:62)                advance
+run_case (solver.hpp:110)              run_case
+tgv_diagnostics (cases.hpp:165)        Solver.tgv_diagnostics
+dissipation_from_series (:208)         dissipation_from_series
+invalid_state_error (core.hpp:58)      InvalidStateError (+ .item/.phase)
+non_positive_dt (integrator.hpp:17)    NonPositiveDtError
+std::invalid_argument                  ConfigError
+=====================================  =====================================
+
+All arithmetic runs in the CUDA library; this module only moves host
+arrays across the ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import HgksConfig
+
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+# ------------------------------------------------------------------- errors
+class HgksError(RuntimeError):
+    pass
+
+
+class InvalidStateError(HgksError):
+    """invalid_state_error: non-positive density or pressure (core.hpp:58-70),
+    message shaped like worker_error (runtime.hpp:37-41)."""
+
+    def __init__(self, msg, item=-1, phase=-1, value=0.0):
+        super().__init__(msg)
+        self.item, self.phase, self.value = item, phase, value
+
+
+class NonPositiveDtError(HgksError):
+    """non_positive_dt (integrator.hpp:17-19)."""
+
+
+class ConfigError(HgksError, ValueError):
+    """configuration error (std::invalid_argument in the reference)."""
+
+
+class CudaError(HgksError):
+    pass
+
+
+def _raise(L, h, rc):
+    msg = L.hgks_last_error(h).decode() if h else "hgks error"
+    if rc == _lib.HGKS_ERR_STATE:
+        code, phase, item, val = ctypes.c_int(), ctypes.c_int(), ctypes.c_long(), ctypes.c_double()
+        L.hgks_error_info(h, ctypes.byref(code), ctypes.byref(phase), ctypes.byref(item), ctypes.byref(val))
+        raise InvalidStateError(msg, item.value, phase.value, val.value)
+    if rc == _lib.HGKS_ERR_DT:
+        raise NonPositiveDtError(msg)
+    if rc == _lib.HGKS_ERR_CONFIG:
+        raise ConfigError(msg)
+    raise CudaError(msg)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if not (a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]):
+        raise TypeError("expected a C-contiguous float64 array")
+    return a.ctypes.data_as(_dp)
+
+
+# ------------------------------------------------------- gas, mesh, scheme
+@dataclass
+class GasModel:
+    """core.hpp:29-43. K = (5 - 3 gamma)/(gamma - 1); mu_ref = 0 is Euler."""
+    gamma: float
+    K: float
+    Pr: float = 1.0
+    mu_ref: float = 0.0
+
+    @staticmethod
+    def make(gamma: float, mu: float = 0.0) -> "GasModel":
+        K = (5.0 - 3.0 * gamma) / (gamma - 1.0)
+        if K < 0.0:
+            raise ConfigError("GasModel: gamma gives negative internal dof")
+        return GasModel(gamma=gamma, K=K, mu_ref=mu)
+
+
+@dataclass
+class Mesh:
+    """mesh.hpp:11-64: periodic box, per-axis node arrays, x fastest."""
+    xs: np.ndarray
+    ys: np.ndarray
+    zs: np.ndarray
+
+    @staticmethod
+    def make(xs, ys, zs) -> "Mesh":
+        xs, ys, zs = (np.ascontiguousarray(a, dtype=np.float64) for a in (xs, ys, zs))
+        for a in (xs, ys, zs):
+            if len(a) < 2 or np.any(np.diff(a) <= 0):
+                raise ConfigError("Mesh: node coordinates must be strictly increasing")
+        return Mesh(xs, ys, zs)
+
+    @property
+    def nx(self):
+        return len(self.xs) - 1
+
+    @property
+    def ny(self):
+        return len(self.ys) - 1
+
+    @property
+    def nz(self):
+        return len(self.zs) - 1
+
+    def ncells(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def cell_index(self, i, j, k):
+        return i + self.nx * (j + self.ny * k)
+
+    def widths(self, c):
+        i, j, k = c % self.nx, (c // self.nx) % self.ny, c // (self.nx * self.ny)
+        return (self.xs[i + 1] - self.xs[i], self.ys[j + 1] - self.ys[j], self.zs[k + 1] - self.zs[k])
+
+    def volume(self, c):
+        h = self.widths(c)
+        return h[0] * h[1] * h[2]
+
+
+def basis_size(degree: int, dim: int) -> int:
+    """BasisSet::N for total degree <= k (basis.hpp:64-82)."""
+    return sum(1 for a in range(degree + 1) for b in range(degree + 1)
+               for c in range(degree + 1 if dim == 3 else 1) if a + b + c <= degree)
+
+
+@dataclass
+class Scheme:
+    """dg.hpp:269-281 (the tables live on the device inside Solver)."""
+    degree: int
+    dim: int
+    gas: GasModel
+    N: int = 0
+
+    @staticmethod
+    def make(degree: int, dim: int, gas: GasModel) -> "Scheme":
+        if degree not in (1, 2, 3):
+            raise ConfigError("build_basis: degree must be 2 or 3 (1 = P1 extension)")
+        if dim not in (2, 3):
+            raise ConfigError("build_basis: dim must be 2 or 3")
+        return Scheme(degree, dim, gas, basis_size(degree, dim))
+
+
+def default_cfl(degree: int) -> float:
+    """integrator.hpp:22 (0.15 for P2, 0.09 otherwise). P1 (extension, unpinned)
+    keeps the reference's formula."""
+    return 0.15 if degree == 2 else 0.09
+
+
+# ------------------------------------------------------------------ solver
+class Solver:
+    """One device-resident DG-HGKS discretisation (mesh + scheme + state),
+    the object behind every call the reference makes per step."""
+
+    def __init__(self, mesh: Mesh, scheme: Scheme, device: int = 0, z_begin: int = 0,
+                 z_count: int = 0):
+        L = _lib.load()
+        self.L = L
+        self.mesh, self.scheme = mesh, scheme
+        self._keep = (mesh.xs, mesh.ys, mesh.zs)
+        cfg = HgksConfig(mesh.nx, mesh.ny, mesh.nz, _ptr(mesh.xs), _ptr(mesh.ys), _ptr(mesh.zs),
+                         scheme.degree, scheme.dim, scheme.gas.gamma, scheme.gas.mu_ref, device,
+                         z_begin, z_count)
+        h = ctypes.c_void_p()
+        rc = L.hgks_create(ctypes.byref(cfg), ctypes.byref(h))
+        self.h = h.value
+        if rc != 0:
+            try:
+                _raise(L, self.h, rc)
+            finally:
+                if self.h:
+                    L.hgks_destroy(self.h)
+                    self.h = None
+        self.N = L.hgks_num_basis(self.h)
+        self.ncoeffs = L.hgks_num_coeffs(self.h)
+        self.z_begin, self.z_count = z_begin, (z_count if z_count > 0 else mesh.nz)
+        self._cbs = []
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.hgks_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, rc):
+        if rc != 0:
+            _raise(self.L, self.h, rc)
+
+    def face_points(self, axis: int) -> int:
+        return self.L.hgks_face_points(self.h, axis)
+
+    # -- state (DGState, dg.hpp:18-38)
+    def set_state(self, coeffs, time: float = 0.0):
+        q = np.ascontiguousarray(coeffs, dtype=np.float64).ravel()
+        if q.size != self.ncoeffs:
+            raise ConfigError(f"state has {q.size} coefficients, expected {self.ncoeffs}")
+        self._check(self.L.hgks_set_state(self.h, _ptr(q), time))
+
+    def get_state(self):
+        q = np.empty(self.ncoeffs)
+        t = ctypes.c_double()
+        self._check(self.L.hgks_get_state(self.h, _ptr(q), ctypes.byref(t)))
+        return q, t.value
+
+    @property
+    def time(self) -> float:
+        t = ctypes.c_double()
+        self._check(self.L.hgks_get_state(self.h, None, ctypes.byref(t)))
+        return t.value
+
+    # -- the hot path
+    def residual(self, dt: float, coeffs=None, faces: bool = False):
+        """residual() (dg.hpp:354): returns {"R", "Rt"[, "faces"]} in the
+        reference layouts (ws.R, ws.Rt, ws.face[a])."""
+        R = np.empty(self.ncoeffs)
+        Rt = np.empty(self.ncoeffs)
+        ncell_owned = self.ncoeffs // (5 * self.N)
+        fb = [np.empty(ncell_owned * self.face_points(a) * 10) for a in range(3)] if faces else [None] * 3
+        c = None if coeffs is None else np.ascontiguousarray(coeffs, dtype=np.float64).ravel()
+        self._check(self.L.hgks_residual(self.h, _ptr(c), dt, _ptr(R), _ptr(Rt), *(_ptr(f) for f in fb)))
+        out = {"R": R, "Rt": Rt}
+        if faces:
+            out["faces"] = fb
+        return out
+
+    def apply_inverse_mass(self, R):
+        R = np.ascontiguousarray(R, dtype=np.float64).ravel()
+        L = np.empty_like(R)
+        self._check(self.L.hgks_apply_inverse_mass(self.h, _ptr(R), _ptr(L)))
+        return L
+
+    def compute_dt(self, cfl: float) -> float:
+        dt = ctypes.c_double()
+        self._check(self.L.hgks_compute_dt(self.h, cfl, ctypes.byref(dt)))
+        return dt.value
+
+    def step(self, dt: float):
+        """two_stage_step on the device-resident state."""
+        self._check(self.L.hgks_step(self.h, dt))
+
+    def two_stage_step_host(self, q: np.ndarray, dt: float):
+        """two_stage_step(q, dt, eval, scratch) on a host vector, in place."""
+        if not (q.dtype == np.float64 and q.flags["C_CONTIGUOUS"] and q.size == self.ncoeffs):
+            raise ConfigError("q must be a contiguous float64 vector of the state size")
+        self._check(self.L.hgks_two_stage_step_host(self.h, _ptr(q), dt))
+
+    def advance_to(self, t_end: float, cfl: float, dt_fixed: float = 0.0, record_interval: float = 0.0) -> int:
+        n = ctypes.c_int()
+        self._check(self.L.hgks_advance(self.h, t_end, cfl, dt_fixed, record_interval, ctypes.byref(n)))
+        return n.value
+
+    # -- cases, diagnostics
+    def project_case(self, case_name: str, t: float = 0.0):
+        self._check(self.L.hgks_project_case(self.h, case_name.encode(), t))
+
+    def tgv_diagnostics(self):
+        """(Ek*vol, enstrophy*vol, vol) sums over owned cells (cases.hpp:165-204)."""
+        e, z, v = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        self._check(self.L.hgks_tgv_diagnostics(self.h, ctypes.byref(e), ctypes.byref(z), ctypes.byref(v)))
+        return e.value, z.value, v.value
+
+    # -- debug / plumbing
+    def set_count_fluxes(self, on: bool = True):
+        self.L.hgks_set_count_fluxes(self.h, int(on))
+
+    def flux_evaluations(self) -> int:
+        return self.L.hgks_flux_evaluations(self.h)
+
+    def launch_count(self) -> int:
+        return self.L.hgks_launch_count(self.h)
+
+    def synchronize(self):
+        self._check(self.L.hgks_synchronize(self.h))
+
+    def set_stream(self, stream_ptr: Optional[int]):
+        self._check(self.L.hgks_set_stream(self.h, stream_ptr))
+
+    def stream(self) -> int:
+        return self.L.hgks_get_stream(self.h) or 0
+
+    def set_kernel_timing(self, on: bool = True):
+        self.L.hgks_set_kernel_timing(self.h, int(on))
+
+    def kernel_times(self):
+        f, c, o = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        self.L.hgks_kernel_times(self.h, ctypes.byref(f), ctypes.byref(c), ctypes.byref(o))
+        return f.value, c.value
+
+    def halo_buffers(self):
+        vals = [ctypes.c_ulonglong() for _ in range(4)]
+        lb, cs, nc = ctypes.c_long(), ctypes.c_long(), ctypes.c_int()
+        self._check(self.L.hgks_halo_buffers(self.h, *(ctypes.byref(v) for v in vals),
+                                             ctypes.byref(lb), ctypes.byref(cs), ctypes.byref(nc)))
+        return {"send_lo": vals[0].value, "send_hi": vals[1].value, "recv_lo": vals[2].value,
+                "recv_hi": vals[3].value, "layer_bytes": lb.value, "comp_stride_bytes": cs.value,
+                "ncomp": nc.value}
+
+    def set_halo_exchange(self, fn: Callable[["Solver"], None]):
+        def cb(user, h):
+            try:
+                fn(self)
+                return 0
+            except Exception:  # noqa: BLE001 — reported as an ABI failure
+                import traceback
+                traceback.print_exc()
+                return 1
+        c = _lib.HALO_FN(cb)
+        self._cbs.append(c)
+        self.L.hgks_set_halo_exchange(self.h, c, None)
+
+    def set_dt_reduce(self, fn: Callable[[float], float]):
+        def cb(user, val):
+            try:
+                val[0] = fn(val[0])
+                return 0
+            except Exception:  # noqa: BLE001
+                import traceback
+                traceback.print_exc()
+                return 1
+        c = _lib.MIN_FN(cb)
+        self._cbs.append(c)
+        self.L.hgks_set_dt_reduce(self.h, c, None)
+
+
+# --------------------------------------------------------------- the cases
+@dataclass
+class CaseConfig:
+    """cases.hpp:12-46."""
+    name: str
+    dim: int = 2
+    n: int = 8
+    nonuniform: bool = False
+    gamma: float = 1.4
+    mach0: float = 0.1
+    reynolds: float = 1600.0
+    eps: float = 5.0
+    t_end: float = 2.0
+
+    @staticmethod
+    def named(name: str, n: int) -> "CaseConfig":
+        table = {"adv2d": (2, 2.0), "adv3d": (3, 2.0), "vortex2d": (2, 10.0), "tgv": (3, 10.0)}
+        if name not in table:
+            raise ConfigError("unknown case: " + name)
+        dim, t_end = table[name]
+        return CaseConfig(name=name, dim=dim, n=n, t_end=t_end)
+
+    def viscosity(self) -> float:
+        return 1.0 / self.reynolds if self.name == "tgv" else 0.0
+
+
+def case_axis_nodes(lo: float, hi: float, n: int, nonuniform: bool) -> np.ndarray:
+    """cases.hpp:50-57: x = xi + 0.05 sin(pi xi) on the uniform parameter nodes."""
+    xi = np.array([lo + (hi - lo) * i / n for i in range(n + 1)])
+    return xi + 0.05 * np.sin(np.pi * xi) if nonuniform else xi
+
+
+def build_mesh(cfg: CaseConfig) -> Mesh:
+    """cases.hpp:59-73 (2-D cases: one z cell spanning the domain)."""
+    if cfg.n < 4:
+        raise ConfigError("build_mesh: need at least 4 cells per axis")
+    lo, hi = 0.0, 2.0
+    if cfg.name == "vortex2d":
+        hi = 10.0
+    if cfg.name == "tgv":
+        lo, hi = -math.pi, math.pi
+    ax = case_axis_nodes(lo, hi, cfg.n, cfg.nonuniform)
+    if cfg.dim == 2:
+        return Mesh.make(ax, ax, np.array([lo, hi]))
+    return Mesh.make(ax, ax.copy(), ax.copy())
+
+
+@dataclass
+class RunOptions:
+    """solver.hpp:10-17."""
+    degree: int = 2
+    cfl: float = 0.0
+    dt_fixed: Optional[float] = None
+    t_end: Optional[float] = None
+    workers: int = 1  # accepted for interface parity; the device ignores it
+    record_interval: float = 0.05
+    device: int = 0
+
+
+@dataclass
+class TgvRecord:
+    t: float
+    Ek: float
+    epsEk: float = 0.0
+    epsZeta: float = 0.0
+
+
+@dataclass
+class RunResult:
+    mesh: Mesh
+    scheme: Scheme
+    solver: Solver
+    steps: int = 0
+    records: List[TgvRecord] = field(default_factory=list)
+
+    @property
+    def state(self):
+        return self.solver.get_state()[0]
+
+
+def setup_run(cfg: CaseConfig, opt: RunOptions, z_begin: int = 0, z_count: int = 0) -> RunResult:
+    """solver.hpp:29-37: mesh, scheme, projected initial state (on device)."""
+    mesh = build_mesh(cfg)
+    scheme = Scheme.make(opt.degree, cfg.dim, GasModel.make(cfg.gamma, cfg.viscosity()))
+    s = Solver(mesh, scheme, device=opt.device, z_begin=z_begin, z_count=z_count)
+    s.project_case(cfg.name, 0.0)
+    return RunResult(mesh, scheme, s)
+
+
+def tgv_record(r: RunResult, reduce: Optional[Callable] = None) -> TgvRecord:
+    """tgv_diagnostics (cases.hpp:165-204); `reduce` sums partials over ranks."""
+    e, z, v = r.solver.tgv_diagnostics()
+    if reduce is not None:
+        e, z, v = reduce((e, z, v))
+    return TgvRecord(t=r.solver.time, Ek=e / v, epsZeta=2.0 * r.scheme.gas.mu_ref * z / v)
+
+
+def advance(r: RunResult, cfg: CaseConfig, opt: RunOptions, on_record: Callable[[RunResult], None]):
+    """solver.hpp:62-108: dt from compute_dt (or dt_fixed), clipped to t_end and
+    the next record; the same full dt drives both residuals; state errors get
+    " at t=<t>" appended."""
+    cfl = opt.cfl if opt.cfl > 0 else default_cfl(opt.degree)
+    t_end = opt.t_end if opt.t_end is not None else cfg.t_end
+    record = cfg.name == "tgv"
+    next_record = opt.record_interval
+    on_record(r)
+    t = r.solver.time
+    while t < t_end - 1e-14 * t_end:
+        dt = opt.dt_fixed if opt.dt_fixed is not None else r.solver.compute_dt(cfl)
+        dt = min(dt, t_end - t)
+        if record:
+            dt = min(dt, next_record - t)
+        try:
+            r.solver.step(dt)
+        except InvalidStateError as e:
+            raise InvalidStateError(f"{e} at t={t:f}", e.item, e.phase, e.value) from None
+        t += dt
+        r.steps += 1
+        if record and t >= next_record - 1e-12:
+            on_record(r)
+            next_record += opt.record_interval
+
+
+def dissipation_from_series(ek, dt):
+    """cases.hpp:208-216."""
+    n = len(ek)
+    if n < 3:
+        raise ConfigError("dissipation_from_series: need at least 3 samples")
+    eps = [0.0] * n
+    eps[0] = -(-3.0 * ek[0] + 4.0 * ek[1] - ek[2]) / (2.0 * dt)
+    for i in range(1, n - 1):
+        eps[i] = -(ek[i + 1] - ek[i - 1]) / (2.0 * dt)
+    eps[n - 1] = -(3.0 * ek[n - 1] - 4.0 * ek[n - 2] + ek[n - 3]) / (2.0 * dt)
+    return eps
+
+
+def run_case(cfg: CaseConfig, opt: RunOptions) -> RunResult:
+    """solver.hpp:110-126."""
+    r = setup_run(cfg, opt)
+
+    def rec(rr):
+        if cfg.name == "tgv":
+            rr.records.append(tgv_record(rr))
+
+    advance(r, cfg, opt, rec)
+    if len(r.records) >= 3:
+        eps = dissipation_from_series([x.Ek for x in r.records], opt.record_interval)
+        for x, e in zip(r.records, eps):
+            x.epsEk = e
+    return r
+
+
+# ------------------------------------------------ free-function spellings
+def residual(solver: Solver, q, dt: float):
+    return solver.residual(dt, coeffs=q)
+
+
+def compute_dt(solver: Solver, cfl: float) -> float:
+    return solver.compute_dt(cfl)
+
+
+def two_stage_step(q: np.ndarray, dt: float, solver: Solver):
+    solver.two_stage_step_host(q, dt)

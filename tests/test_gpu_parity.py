@@ -1,0 +1,190 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Oracle = the reference headers compiled unmodified (oracle/_ref) when that
+build is present, else the C restatement (oracle/hgks_oracle.c, itself pinned
+bitwise to the reference in test_oracle.py). Bar (north_star):
+norm-relative L-inf max|a-b|/max|b| <= 1e-10 on modal coefficients after N
+steps; residual-level R <= 1e-12, Rt <= 1e-10 (Rt carries the reference's own
+If - 2 Ih cancellation, ~4 eps/dt).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_STATE = 1e-10
+TOL_R = 1e-12
+TOL_RT = 1e-10
+
+
+def rel(a, b):
+    d = np.max(np.abs(b))
+    return float(np.max(np.abs(a - b)) / (d if d > 0 else 1.0))
+
+
+def make_pair(P, O, case, n, degree, nonuniform=False):
+    """(device solver, oracle) on the same mesh and the same initial state."""
+    cfg = P.CaseConfig.named(case, n)
+    cfg.nonuniform = nonuniform
+    opt = P.RunOptions(degree=degree)
+    r = P.setup_run(cfg, opt)
+    if O.ref_available():
+        ref = O.RefRun(case, n, degree, nonuniform=nonuniform, workers=2)
+        q0, _ = ref.get_state()
+    else:
+        ref = O.Oracle(case, n, degree, nonuniform=nonuniform)
+        q0 = ref.state.copy()
+    r.solver.set_state(q0, 0.0)
+    return r, ref, q0
+
+
+CASES = [
+    ("adv3d", 4, 2, True),
+    ("adv3d", 6, 2, False),
+    ("tgv", 4, 2, False),
+    ("tgv", 8, 2, False),
+    ("tgv", 4, 3, False),
+    ("adv3d", 4, 3, True),
+    ("adv2d", 6, 2, True),
+    ("vortex2d", 6, 3, False),
+]
+
+
+@pytest.mark.parametrize("case,n,degree,nonuni", CASES)
+def test_residual_matches_oracle(hgks, oracle_mod, case, n, degree, nonuni):
+    P, O = hgks, oracle_mod
+    r, ref, q0 = make_pair(P, O, case, n, degree, nonuni)
+    dt = ref.compute_dt(0.15 if degree == 2 else 0.09)
+    a = ref.residual(dt, faces=True)
+    b = r.solver.residual(dt, faces=True)
+    assert rel(b["R"], a["R"]) <= TOL_R
+    assert rel(b["Rt"], a["Rt"]) <= TOL_RT
+    for fa, fb in zip(a["faces"], b["faces"]):
+        F_ref = fa.reshape(-1, 10)
+        F_dev = fb.reshape(-1, 10)
+        assert rel(F_dev[:, :5], F_ref[:, :5]) <= TOL_R
+        assert rel(F_dev[:, 5:], F_ref[:, 5:]) <= TOL_RT
+
+
+@pytest.mark.parametrize("case,n,degree,nonuni", CASES)
+def test_steps_match_oracle(hgks, oracle_mod, case, n, degree, nonuni):
+    P, O = hgks, oracle_mod
+    r, ref, q0 = make_pair(P, O, case, n, degree, nonuni)
+    cfl = 0.15 if degree == 2 else 0.09
+    for _ in range(10):
+        dt = ref.compute_dt(cfl)
+        dt_dev = r.solver.compute_dt(cfl)
+        assert abs(dt_dev - dt) <= 1e-12 * dt
+        ref.step(dt)
+        r.solver.step(dt)  # identical dt sequence (SURVEY §8a gotcha 8)
+    q_ref = ref.get_state()[0] if hasattr(ref, "get_state") else ref.state
+    q_dev, t = r.solver.get_state()
+    assert rel(q_dev, q_ref) <= TOL_STATE
+    # per conserved variable as well
+    N = r.solver.N
+    for v in range(5):
+        assert rel(q_dev.reshape(-1, N, 5)[:, :, v], q_ref.reshape(-1, N, 5)[:, :, v]) <= 1e-8
+
+
+def test_projection_matches_oracle(hgks, oracle_mod):
+    P, O = hgks, oracle_mod
+    for case, n, deg in [("tgv", 6, 2), ("adv3d", 4, 3), ("vortex2d", 6, 2)]:
+        cfg = P.CaseConfig.named(case, n)
+        r = P.setup_run(cfg, P.RunOptions(degree=deg))
+        o = O.Oracle(case, n, deg)
+        assert rel(r.solver.get_state()[0], o.state) <= 1e-13
+
+
+def test_flux_count_each_face_once(hgks):
+    """test_runtime.cpp:63-78: each interior face flux computed exactly once."""
+    P = hgks
+    r = P.setup_run(P.CaseConfig.named("adv3d", 6), P.RunOptions(degree=2))
+    r.solver.set_count_fluxes(True)
+    r.solver.residual(1e-3)
+    expected = sum(r.mesh.ncells() * r.solver.face_points(a) for a in range(3))
+    assert r.solver.flux_evaluations() == expected
+    r.solver.residual(1e-3)
+    assert r.solver.flux_evaluations() == 2 * expected
+
+
+def test_bitwise_repeatable(hgks):
+    """test_runtime.cpp:80-115 analogue: no atomics on the data path."""
+    P = hgks
+    out = []
+    for _ in range(2):
+        r = P.setup_run(P.CaseConfig.named("tgv", 8), P.RunOptions(degree=2))
+        for _ in range(3):
+            r.solver.step(r.solver.compute_dt(0.15))
+        out.append(r.solver.get_state()[0])
+    assert np.array_equal(out[0], out[1])
+
+
+def test_two_stage_step_host_dropin(hgks, oracle_mod):
+    P, O = hgks, oracle_mod
+    r, ref, q0 = make_pair(P, O, "tgv", 4, 2)
+    dt = ref.compute_dt(0.15)
+    q = q0.copy()
+    r.solver.two_stage_step_host(q, dt)
+    ref.step(dt)
+    q_ref = ref.get_state()[0] if hasattr(ref, "get_state") else ref.state
+    assert rel(q, q_ref) <= TOL_STATE
+
+
+def test_blowup_message_names_pressure(hgks, oracle_mod):
+    """test_solver.cpp:122-140: poisoned cell -> diagnosable error; the same
+    item and message as the reference."""
+    P, O = hgks, oracle_mod
+    cfg = P.CaseConfig.named("adv3d", 6)
+    r = P.setup_run(cfg, P.RunOptions(degree=2))
+    q, _ = r.solver.get_state()
+    N = r.solver.N
+    q = q.reshape(-1, N, 5)
+    q[2, 0, 0] = 1.0
+    q[2, 0, 1] = 10.0
+    q[2, 0, 4] = 1.0
+    q = q.ravel().copy()
+    r.solver.set_state(q)
+    o = O.Oracle("adv3d", 6, 2)
+    o.set_state(q)
+    with pytest.raises(O.OracleError) as eo:
+        o.residual(1e-3)
+    with pytest.raises(P.InvalidStateError) as ed:
+        r.solver.residual(1e-3)
+    assert "pressure" in str(ed.value)
+    assert ed.value.item == eo.value.item
+    assert str(ed.value).split(":")[0] == str(eo.value).split(":")[0]  # "item <i>"
+    # the offending value agrees to print precision
+    assert abs(ed.value.value - eo.value.value) <= 1e-9 * max(1.0, abs(eo.value.value))
+    # compute_dt on a poisoned mean throws the bare state error
+    with pytest.raises((P.InvalidStateError, P.NonPositiveDtError)):
+        r.solver.compute_dt(0.15)
+
+
+def test_free_stream_steady(hgks):
+    """test_solver.cpp:55-75: uniform state on a nonuniform mesh stays put."""
+    P = hgks
+    cfg = P.CaseConfig.named("adv3d", 6)
+    cfg.nonuniform = True
+    r = P.setup_run(cfg, P.RunOptions(degree=3))
+    rho, U, V, W, lam = 1.1, 0.4, -0.7, 0.2, 0.6
+    p = 0.5 * rho / lam
+    E = p / 0.4 + 0.5 * rho * (U * U + V * V + W * W)
+    N = r.solver.N
+    q = np.zeros((r.mesh.ncells(), N, 5))
+    q[:, 0, :] = [rho, rho * U, rho * V, rho * W, E]
+    q = q.ravel()
+    r.solver.set_state(q)
+    for _ in range(5):
+        r.solver.step(r.solver.compute_dt(0.09))
+    assert np.max(np.abs(r.solver.get_state()[0] - q)) <= 1e-12
+
+
+def test_tgv_diagnostics_match(hgks, oracle_mod):
+    P, O = hgks, oracle_mod
+    r = P.setup_run(P.CaseConfig.named("tgv", 8), P.RunOptions(degree=2))
+    rec = P.tgv_record(r)
+    o = O.Oracle("tgv", 8, 2)
+    ek, epsz = o.tgv_diagnostics()
+    assert abs(rec.Ek - ek) <= 1e-13 * ek
+    assert abs(rec.epsZeta - epsz) <= 1e-12 * epsz
+    assert abs(rec.Ek - 0.125) <= 0.125 * 1e-3  # test_cases.cpp:140-150
