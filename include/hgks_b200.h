@@ -115,17 +115,30 @@ int hgks_project_case(hgks_solver* s, const char* case_name, double t);
 int hgks_tgv_diagnostics(hgks_solver* s, double* ek_vol, double* ens_vol, double* volume);
 
 /* ---- multi-GPU z-slabs. The halo is one layer of cell
- * coefficients below and above the owned slab. */
-/* device pointers (as integers) and byte size of the owned bottom / top
- * layers (send) and ghost bottom / top layers (receive) of the array that is
- * the input of the next residual; valid until the next call. */
+ * coefficients below and above the owned slab, packed contiguously:
+ * [comp][cell-in-layer], hgks_halo_bytes() per direction. */
+long hgks_halo_bytes(const hgks_solver* s);
+/* device pointers (as integers) of the solver-owned contiguous halo buffers:
+ * send_lo/send_hi hold the packed bottom/top owned layers, recv_lo/recv_hi
+ * receive the neighbours' layers. */
 int hgks_halo_buffers(hgks_solver* s, unsigned long long* send_lo, unsigned long long* send_hi,
-                      unsigned long long* recv_lo, unsigned long long* recv_hi,
-                      long* layer_bytes, long* comp_stride_bytes, int* ncomp);
-/* callback run at each exchange point, on the solver's stream; returns 0 on
- * success. Without one, ghosts are filled by the periodic wrap (single slab). */
-typedef int (*hgks_halo_fn)(void* user, hgks_solver* s);
+                      unsigned long long* recv_lo, unsigned long long* recv_hi);
+/* which = 0: the state q^n, 1: the stage array q*. pack: owned boundary
+ * layers -> send buffers; unpack: recv buffers -> ghost layers. Both are
+ * kernels on the solver stream. */
+int hgks_halo_pack(hgks_solver* s, int which);
+int hgks_halo_unpack(hgks_solver* s, int which);
+/* callback run at each exchange point (after pack, before unpack), on the
+ * solver's stream; moves send_lo -> lower neighbour's recv_hi and send_hi ->
+ * upper neighbour's recv_lo; returns 0 on success. Without one, a multi-slab
+ * hgks_step fails; a single slab fills its ghosts by the periodic wrap. */
+typedef int (*hgks_halo_fn)(void* user, hgks_solver* s, int which);
 void hgks_set_halo_exchange(hgks_solver* s, hgks_halo_fn fn, void* user);
+/* Split-phase step for callers that drive the exchange themselves (several
+ * slabs in one process): phase 0 = stage 1 (needs q^n ghosts), phase 1 =
+ * stage 2 (needs q* ghosts), phase 2 = error check + commit. A single slab
+ * fills its own ghosts; a multi-slab solver expects them unpacked already. */
+int hgks_step_phase(hgks_solver* s, double dt, int phase);
 /* dt reduction hook for multi-slab runs: min over ranks (order independent). */
 typedef int (*hgks_min_fn)(void* user, double* value);
 void hgks_set_dt_reduce(hgks_solver* s, hgks_min_fn fn, void* user);
@@ -140,6 +153,11 @@ long hgks_launch_count(const hgks_solver* s);
  * the solver stream) when timing is enabled */
 void hgks_set_kernel_timing(hgks_solver* s, int on);
 int hgks_kernel_times(hgks_solver* s, double* face_ms, double* cell_ms, double* other_ms);
+
+/* Roofline denominator: sustained FP64 FMA throughput of `device`, measured
+ * with a DFMA-chain kernel over ~`ms` milliseconds (CUDA events). Writes
+ * TFLOP/s (2 flops per DFMA). */
+int hgks_measure_fp64_peak(int device, double ms, double* tflops);
 
 #ifdef __cplusplus
 }

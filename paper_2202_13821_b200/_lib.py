@@ -25,9 +25,10 @@ EXPORTS = [
     "hgks_num_basis", "hgks_num_coeffs", "hgks_face_points", "hgks_set_state", "hgks_get_state",
     "hgks_residual", "hgks_apply_inverse_mass", "hgks_compute_dt", "hgks_step",
     "hgks_two_stage_step_host", "hgks_advance", "hgks_set_count_fluxes", "hgks_flux_evaluations",
-    "hgks_project_case", "hgks_tgv_diagnostics", "hgks_halo_buffers", "hgks_set_halo_exchange",
+    "hgks_project_case", "hgks_tgv_diagnostics", "hgks_halo_bytes", "hgks_halo_buffers",
+    "hgks_halo_pack", "hgks_halo_unpack", "hgks_set_halo_exchange", "hgks_step_phase",
     "hgks_set_dt_reduce", "hgks_set_stream", "hgks_get_stream", "hgks_synchronize",
-    "hgks_launch_count", "hgks_set_kernel_timing", "hgks_kernel_times",
+    "hgks_launch_count", "hgks_set_kernel_timing", "hgks_kernel_times", "hgks_measure_fp64_peak",
 ]
 
 
@@ -41,7 +42,7 @@ class HgksConfig(ctypes.Structure):
     ]
 
 
-HALO_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p)
+HALO_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int)
 MIN_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, _dp)
 
 _lib = None
@@ -84,7 +85,13 @@ def load():
     L.hgks_flux_evaluations.restype = ctypes.c_long
     L.hgks_project_case.argtypes = [sp, ctypes.c_char_p, ctypes.c_double]
     L.hgks_tgv_diagnostics.argtypes = [sp, _dp, _dp, _dp]
-    L.hgks_halo_buffers.argtypes = [sp, _u64p, _u64p, _u64p, _u64p, _lp, _lp, _ip]
+    L.hgks_halo_bytes.argtypes = [sp]
+    L.hgks_halo_bytes.restype = ctypes.c_long
+    L.hgks_halo_buffers.argtypes = [sp, _u64p, _u64p, _u64p, _u64p]
+    L.hgks_halo_pack.argtypes = [sp, ctypes.c_int]
+    L.hgks_halo_unpack.argtypes = [sp, ctypes.c_int]
+    L.hgks_step_phase.argtypes = [sp, ctypes.c_double, ctypes.c_int]
+    L.hgks_measure_fp64_peak.argtypes = [ctypes.c_int, ctypes.c_double, _dp]
     L.hgks_set_halo_exchange.argtypes = [sp, HALO_FN, sp]
     L.hgks_set_halo_exchange.restype = None
     L.hgks_set_dt_reduce.argtypes = [sp, MIN_FN, sp]

@@ -128,6 +128,42 @@ __global__ void ghost_wrap_kernel(KParams kp, double* q, int ncomp) {
     }
 }
 
+// halo layers <-> contiguous buffers [send_lo|send_hi|recv_lo|recv_hi][comp][S]
+__global__ void halo_pack_kernel(KParams kp, const double* __restrict__ a, double* __restrict__ buf, int NC) {
+    const long L = (long)kp.S * NC;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < L; e += (long)gridDim.x * blockDim.x) {
+        const long comp = e / kp.S, c = e - comp * kp.S;
+        buf[e] = a[comp * kp.cs + kp.S + c];                      // owned layer 0
+        buf[L + e] = a[comp * kp.cs + (long)kp.nzl * kp.S + c];  // owned layer nzl-1
+    }
+}
+
+__global__ void halo_unpack_kernel(KParams kp, double* __restrict__ a, const double* __restrict__ buf, int NC) {
+    const long L = (long)kp.S * NC;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < L; e += (long)gridDim.x * blockDim.x) {
+        const long comp = e / kp.S, c = e - comp * kp.S;
+        a[comp * kp.cs + c] = buf[2 * L + e];                                // ghost below
+        a[comp * kp.cs + (long)(kp.nzl + 1) * kp.S + c] = buf[3 * L + e];   // ghost above
+    }
+}
+
+// FP64 pipe peak: DFMA_CHAINS independent dependency chains per thread
+#define DFMA_CHAINS 8
+__global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters) {
+    double a[DFMA_CHAINS];
+#pragma unroll
+    for (int k = 0; k < DFMA_CHAINS; ++k) a[k] = threadIdx.x * 1e-3 + k;
+    const double b = 0.999999, c = 1e-7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < DFMA_CHAINS; ++k) a[k] = fma(a[k], b, c);
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < DFMA_CHAINS; ++k) s += a[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 enum : int { CASE_ADV2D = 0, CASE_ADV3D = 1, CASE_VORTEX2D = 2, CASE_TGV = 3 };
 
 struct CaseParams {

@@ -56,7 +56,8 @@ struct hgks_solver {
     void* halo_user = nullptr;
     hgks_min_fn dtmin = nullptr;
     void* dtmin_user = nullptr;
-    const double* halo_array = nullptr;  // array whose ghosts the next exchange fills
+    double* d_halo = nullptr;  // [4][NC][S]: send_lo, send_hi, recv_lo, recv_hi
+    bool external_halo = false;  // hgks_step_phase: caller exchanges ghosts
     bool count_fluxes = false;
     long flux_evals = 0;
     long launches = 0;
@@ -143,23 +144,47 @@ std::string fmt_f(double v) {  // std::to_string(double) == "%f"
     return b;
 }
 
-// fill ghost layers of array a before a residual: periodic wrap for a single
-// slab, the user's halo exchange otherwise
-int fill_ghosts(hgks_solver* s, double* a) {
+double* which_array(hgks_solver* s, int which) { return which == 0 ? s->qa : s->qs; }
+
+int halo_pack(hgks_solver* s, int which) {
+    KParams kp = make_params(s, 0.0, 0);
+    const long total = s->S * s->NC;
+    const int blocks = (int)std::min<long>((total + 255) / 256, 148L * 16);
+    halo_pack_kernel<<<blocks, 256, 0, s->stream>>>(kp, which_array(s, which), s->d_halo, s->NC);
+    ++s->launches;
+    CK(cudaGetLastError());
+    return HGKS_OK;
+}
+
+int halo_unpack(hgks_solver* s, int which) {
+    KParams kp = make_params(s, 0.0, 0);
+    const long total = s->S * s->NC;
+    const int blocks = (int)std::min<long>((total + 255) / 256, 148L * 16);
+    halo_unpack_kernel<<<blocks, 256, 0, s->stream>>>(kp, which_array(s, which), s->d_halo, s->NC);
+    ++s->launches;
+    CK(cudaGetLastError());
+    return HGKS_OK;
+}
+
+// fill ghost layers of array `which` before a residual: periodic wrap for a
+// single slab; pack -> user exchange -> unpack for a slab of a multi-slab run
+// (skipped when the caller drives the exchange through hgks_step_phase)
+int fill_ghosts(hgks_solver* s, int which) {
     if (s->single) {
         KParams kp = make_params(s, 0.0, 0);
         const long total = s->S * s->NC * 2;
         const int blocks = (int)std::min<long>((total + 255) / 256, 148L * 16);
-        ghost_wrap_kernel<<<blocks, 256, 0, s->stream>>>(kp, a, s->NC);
+        ghost_wrap_kernel<<<blocks, 256, 0, s->stream>>>(kp, which_array(s, which), s->NC);
         ++s->launches;
         CK(cudaGetLastError());
         return HGKS_OK;
     }
+    if (s->external_halo) return HGKS_OK;
     if (!s->halo) return fail(s, HGKS_ERR_CONFIG, "multi-slab solver has no halo exchange set");
-    s->halo_array = a;
-    const int rc = s->halo(s->halo_user, s);
-    if (rc != 0) return fail(s, HGKS_ERR_CUDA, "halo exchange callback failed");
-    return HGKS_OK;
+    int rc = halo_pack(s, which);
+    if (rc) return rc;
+    if (s->halo(s->halo_user, s, which) != 0) return fail(s, HGKS_ERR_CUDA, "halo exchange callback failed");
+    return halo_unpack(s, which);
 }
 
 int reset_error(hgks_solver* s) {
@@ -220,9 +245,10 @@ void ev_record(hgks_solver* s, int i) {
 }
 
 // One residual evaluation of `in` (ghosts filled here) in the given mode.
-int run_residual(hgks_solver* s, double* in, double dt, int stage, int mode, const double* qn,
+int run_residual(hgks_solver* s, int which, double dt, int stage, int mode, const double* qn,
                  double* o0, double* o1, double* o2) {
-    int rc = fill_ghosts(s, in);
+    double* in = which_array(s, which);
+    int rc = fill_ghosts(s, which);
     if (rc) return rc;
     KParams kp = make_params(s, dt, stage);
     ev_record(s, stage * 3 + 0);
@@ -347,13 +373,15 @@ int hgks_create(const hgks_config* cfg, hgks_solver** out) {
     CK(cudaMemset(s->d_key, 0, 4 * sizeof(unsigned long long)));
     CK(cudaMalloc(&s->d_val, 4 * sizeof(double)));
     CK(cudaMalloc(&s->d_red, 4096 * sizeof(double)));
+    CK(cudaMalloc(&s->d_halo, 4 * (size_t)s->S * s->NC * sizeof(double)));
+    CK(cudaMemset(s->d_halo, 0, 4 * (size_t)s->S * s->NC * sizeof(double)));
     return HGKS_OK;
 }
 
 void hgks_destroy(hgks_solver* s) {
     if (!s) return;
     for (double* p : {s->d_tab, s->d_dx, s->d_dy, s->d_dz, s->qa, s->qb, s->qs, s->L1, s->Lt1,
-                      s->R, s->Rt, s->tmp, s->face[0], s->face[1], s->face[2], s->d_val, s->d_red})
+                      s->R, s->Rt, s->tmp, s->face[0], s->face[1], s->face[2], s->d_val, s->d_red, s->d_halo})
         if (p) cudaFree(p);
     if (s->d_key) cudaFree(s->d_key);
     for (auto& e : s->ev)
@@ -424,15 +452,16 @@ int download_faces(hgks_solver* s, int axis, double* host) {
     return HGKS_OK;
 }
 
-int do_step(hgks_solver* s, double dt) {
-    int rc = reset_error(s);
-    if (rc) return rc;
-    // stage 1: L1, Lt1, q* from q^n (qa)
-    rc = run_residual(s, s->qa, dt, 0, MODE_STAGE1, nullptr, s->qs, s->L1, s->Lt1);
-    if (rc) return rc;
-    // stage 2: q^{n+1} into qb from q*, q^n, L1, Lt1
-    rc = run_residual(s, s->qs, dt, 1, MODE_STAGE2, s->qa, s->qb, nullptr, nullptr);
-    if (rc) return rc;
+int step_phase(hgks_solver* s, double dt, int phase) {
+    int rc;
+    if (phase == 0) {
+        // stage 1: L1, Lt1, q* from q^n (qa)
+        rc = reset_error(s);
+        if (rc) return rc;
+        return run_residual(s, 0, dt, 0, MODE_STAGE1, nullptr, s->qs, s->L1, s->Lt1);
+    }
+    if (phase == 1)  // stage 2: q^{n+1} into qb from q*, q^n, L1, Lt1
+        return run_residual(s, 1, dt, 1, MODE_STAGE2, s->qa, s->qb, nullptr, nullptr);
     const double* inputs[2] = {s->qa, s->qs};
     bool failed = false;
     rc = check_error(s, inputs, dt, &failed);
@@ -440,6 +469,14 @@ int do_step(hgks_solver* s, double dt) {
     collect_times(s, 2);
     std::swap(s->qa, s->qb);
     s->time += dt;
+    return HGKS_OK;
+}
+
+int do_step(hgks_solver* s, double dt) {
+    for (int ph = 0; ph < 3; ++ph) {
+        const int rc = step_phase(s, dt, ph);
+        if (rc) return rc;
+    }
     return HGKS_OK;
 }
 
@@ -465,16 +502,17 @@ int hgks_residual(hgks_solver* s, const double* coeffs, double dt, double* R, do
     const size_t arr = (size_t)s->NC * s->cs * sizeof(double);
     if (!s->R) CK(cudaMalloc(&s->R, arr));
     if (!s->Rt) CK(cudaMalloc(&s->Rt, arr));
-    double* in = s->qa;
+    int which = 0;
     int rc;
     if (coeffs) {
         rc = upload_aos(s, coeffs, s->qs);
         if (rc) return rc;
-        in = s->qs;
+        which = 1;
     }
+    const double* in = which_array(s, which);
     rc = reset_error(s);
     if (rc) return rc;
-    rc = run_residual(s, in, dt, 0, MODE_RESIDUAL, nullptr, s->R, s->Rt, nullptr);
+    rc = run_residual(s, which, dt, 0, MODE_RESIDUAL, nullptr, s->R, s->Rt, nullptr);
     if (rc) return rc;
     const double* inputs[2] = {in, in};
     bool failed = false;
@@ -644,19 +682,27 @@ int hgks_tgv_diagnostics(hgks_solver* s, double* ek_vol, double* ens_vol, double
     return HGKS_OK;
 }
 
+long hgks_halo_bytes(const hgks_solver* s) { return s->S * s->NC * (long)sizeof(double); }
+
 int hgks_halo_buffers(hgks_solver* s, unsigned long long* send_lo, unsigned long long* send_hi,
-                      unsigned long long* recv_lo, unsigned long long* recv_hi, long* layer_bytes,
-                      long* comp_stride_bytes, int* ncomp) {
-    const double* a = s->halo_array ? s->halo_array : s->qa;
-    const size_t L = (size_t)s->S;
-    if (send_lo) *send_lo = (unsigned long long)(a + L);
-    if (send_hi) *send_hi = (unsigned long long)(a + (size_t)s->nzl * L);
-    if (recv_lo) *recv_lo = (unsigned long long)(a);
-    if (recv_hi) *recv_hi = (unsigned long long)(a + (size_t)(s->nzl + 1) * L);
-    if (layer_bytes) *layer_bytes = (long)(L * sizeof(double));
-    if (comp_stride_bytes) *comp_stride_bytes = (long)(s->cs * sizeof(double));
-    if (ncomp) *ncomp = s->NC;
+                      unsigned long long* recv_lo, unsigned long long* recv_hi) {
+    const size_t L = (size_t)s->S * s->NC;
+    if (send_lo) *send_lo = (unsigned long long)(s->d_halo);
+    if (send_hi) *send_hi = (unsigned long long)(s->d_halo + L);
+    if (recv_lo) *recv_lo = (unsigned long long)(s->d_halo + 2 * L);
+    if (recv_hi) *recv_hi = (unsigned long long)(s->d_halo + 3 * L);
     return HGKS_OK;
+}
+
+int hgks_halo_pack(hgks_solver* s, int which) { return halo_pack(s, which); }
+int hgks_halo_unpack(hgks_solver* s, int which) { return halo_unpack(s, which); }
+
+int hgks_step_phase(hgks_solver* s, double dt, int phase) {
+    if (phase < 0 || phase > 2) return fail(s, HGKS_ERR_CONFIG, "hgks_step_phase: phase must be 0, 1 or 2");
+    s->external_halo = true;
+    const int rc = step_phase(s, dt, phase);
+    s->external_halo = false;
+    return rc;
 }
 
 void hgks_set_halo_exchange(hgks_solver* s, hgks_halo_fn fn, void* user) {
@@ -699,6 +745,44 @@ int hgks_kernel_times(hgks_solver* s, double* face_ms, double* cell_ms, double* 
     if (face_ms) *face_ms = s->t_face;
     if (cell_ms) *cell_ms = s->t_cell;
     if (other_ms) *other_ms = s->t_other;
+    return HGKS_OK;
+}
+
+int hgks_measure_fp64_peak(int device, double ms, double* tflops) {
+    hgks_solver* s = nullptr;  // for CK
+    CK(cudaSetDevice(device));
+    const int blocks = 148 * 8, threads = 256;
+    double* out = nullptr;
+    CK(cudaMalloc(&out, (size_t)blocks * threads * sizeof(double)));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    int iters = 4096;
+    float t = 0.f;
+    for (int pass = 0; pass < 6; ++pass) {  // grow iters until the launch lasts ~ms
+        CK(cudaEventRecord(e0));
+        dfma_peak_kernel<<<blocks, threads>>>(out, iters);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(&t, e0, e1));
+        if (t >= ms * 0.5) break;
+        iters = (int)std::min(1.0e8, iters * std::max(2.0, ms / std::max(t, 0.01f)));
+    }
+    // best of three at the final size
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        CK(cudaEventRecord(e0));
+        dfma_peak_kernel<<<blocks, threads>>>(out, iters);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(&t, e0, e1));
+        best = std::min(best, t);
+    }
+    const double flops = 2.0 * DFMA_CHAINS * (double)iters * blocks * threads;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
     return HGKS_OK;
 }
 

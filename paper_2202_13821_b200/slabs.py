@@ -1,0 +1,114 @@
+"""z-slab domain decomposition of the periodic box across ranks.
+
+The reference has no distributed path (MPI is out of scope); its
+only parallelism is contiguous index ranges per worker
+(runtime.hpp:17-35). Here each rank owns a contiguous range of z layers
+(contiguous in the x-fastest cell index, mesh.hpp:34); one layer of cell
+coefficients moves to each z neighbour per stage, and each rank computes the
+flux of its top boundary face redundantly from identical inputs, so results
+are bitwise identical for any rank count. dt is a min-allreduce (order
+independent, exact).
+
+Transport is torch.distributed (NCCL on GPUs, gloo on CPU for tests): the
+solver packs its boundary layers into contiguous device buffers
+(hgks_halo_pack), this module moves them, the solver unpacks
+(hgks_halo_unpack) — all on one stream.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Tuple
+
+
+def slab_partition(nz: int, world: int) -> List[Tuple[int, int]]:
+    """(z_begin, z_count) per rank: contiguous, the first nz % world ranks
+    one layer larger (the reference's Partition::make rule, runtime.hpp:21-34)."""
+    if world < 1:
+        raise ValueError("slab_partition: world must be >= 1")
+    if nz < world:
+        raise ValueError(f"slab_partition: {nz} z layers cannot feed {world} ranks")
+    base, rem = divmod(nz, world)
+    out, z = [], 0
+    for r in range(world):
+        n = base + (1 if r < rem else 0)
+        out.append((z, n))
+        z += n
+    return out
+
+
+def ring_neighbors(rank: int, world: int) -> Tuple[int, int]:
+    """(lower, upper) z neighbours on the periodic ring."""
+    return (rank - 1) % world, (rank + 1) % world
+
+
+def device_view(ptr: int, nbytes: int, device: int):
+    """Zero-copy torch view of a device buffer owned by the C library."""
+    import torch
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (nbytes // 8,), "typestr": "<f8", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+
+    return torch.as_tensor(_CAI(), device=f"cuda:{device}")
+
+
+def exchange_halos(send_lo, send_hi, recv_lo, recv_hi, rank: int, world: int, group=None):
+    """send_lo -> lower neighbour's recv_hi, send_hi -> upper neighbour's recv_lo.
+
+    Posting order is the same on every rank (down-going pair first), so for
+    world == 2 — where lower == upper — point-to-point messages still match
+    in order under NCCL (which ignores tags) and gloo (tags 0/1)."""
+    import torch.distributed as dist
+
+    if world == 1:
+        recv_hi.copy_(send_lo)
+        recv_lo.copy_(send_hi)
+        return
+    lower, upper = ring_neighbors(rank, world)
+    ops = [
+        dist.P2POp(dist.isend, send_lo, lower, group, 0),
+        dist.P2POp(dist.irecv, recv_hi, upper, group, 0),
+        dist.P2POp(dist.isend, send_hi, upper, group, 1),
+        dist.P2POp(dist.irecv, recv_lo, lower, group, 1),
+    ]
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+
+
+def min_allreduce(value: float, device: Optional[str] = None, group=None) -> float:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return float(t.item())
+
+
+def sum_allreduce(values, device: Optional[str] = None, group=None):
+    """Fixed-order sum over ranks: gather every rank's partials, add in rank
+    order (deterministic, SURVEY §5 'per record')."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, t, group=group)
+    acc = [0.0] * len(values)
+    for o in out:
+        for i, v in enumerate(o.tolist()):
+            acc[i] += v
+    return acc
+
+
+def attach(solver, rank: int, world: int, device: int, group=None):
+    """Wire a slab solver to torch.distributed: halo exchange on the solver's
+    stream (which must be torch's current stream) and min-allreduce of dt."""
+    nbytes = solver.halo_bytes()
+    ptrs = solver.halo_buffers()
+    views = [device_view(p, nbytes, device) for p in ptrs]
+
+    def exchange(_s, _which):
+        exchange_halos(views[0], views[1], views[2], views[3], rank, world, group)
+
+    solver.set_halo_exchange(exchange)
+    solver.set_dt_reduce(lambda v: min_allreduce(v, device=f"cuda:{device}", group=group))
+    return views

@@ -319,19 +319,31 @@ class Solver:
         self.L.hgks_kernel_times(self.h, ctypes.byref(f), ctypes.byref(c), ctypes.byref(o))
         return f.value, c.value
 
-    def halo_buffers(self):
-        vals = [ctypes.c_ulonglong() for _ in range(4)]
-        lb, cs, nc = ctypes.c_long(), ctypes.c_long(), ctypes.c_int()
-        self._check(self.L.hgks_halo_buffers(self.h, *(ctypes.byref(v) for v in vals),
-                                             ctypes.byref(lb), ctypes.byref(cs), ctypes.byref(nc)))
-        return {"send_lo": vals[0].value, "send_hi": vals[1].value, "recv_lo": vals[2].value,
-                "recv_hi": vals[3].value, "layer_bytes": lb.value, "comp_stride_bytes": cs.value,
-                "ncomp": nc.value}
+    # -- multi-slab plumbing
+    def halo_bytes(self) -> int:
+        return self.L.hgks_halo_bytes(self.h)
 
-    def set_halo_exchange(self, fn: Callable[["Solver"], None]):
-        def cb(user, h):
+    def halo_buffers(self):
+        """device addresses of the packed halo buffers (send_lo, send_hi, recv_lo, recv_hi)."""
+        vals = [ctypes.c_ulonglong() for _ in range(4)]
+        self._check(self.L.hgks_halo_buffers(self.h, *(ctypes.byref(v) for v in vals)))
+        return tuple(v.value for v in vals)
+
+    def halo_pack(self, which: int):
+        self._check(self.L.hgks_halo_pack(self.h, which))
+
+    def halo_unpack(self, which: int):
+        self._check(self.L.hgks_halo_unpack(self.h, which))
+
+    def step_phase(self, dt: float, phase: int):
+        self._check(self.L.hgks_step_phase(self.h, dt, phase))
+
+    def set_halo_exchange(self, fn: Callable[["Solver", int], None]):
+        """fn(solver, which) moves send_lo -> lower neighbour recv_hi and
+        send_hi -> upper neighbour recv_lo (on the solver's stream)."""
+        def cb(user, h, which):
             try:
-                fn(self)
+                fn(self, which)
                 return 0
             except Exception:  # noqa: BLE001 — reported as an ABI failure
                 import traceback
@@ -353,6 +365,17 @@ class Solver:
         c = _lib.MIN_FN(cb)
         self._cbs.append(c)
         self.L.hgks_set_dt_reduce(self.h, c, None)
+
+
+def measure_fp64_peak(device: int = 0, ms: float = 50.0) -> float:
+    """Sustained DFMA throughput (TFLOP/s) of the device: the FP64 roofline
+    denominator (MEASURED_PEAKS.json has no FP64 entry)."""
+    L = _lib.load()
+    t = ctypes.c_double()
+    rc = L.hgks_measure_fp64_peak(device, ms, ctypes.byref(t))
+    if rc != 0:
+        raise CudaError("fp64 peak measurement failed")
+    return t.value
 
 
 # --------------------------------------------------------------- the cases
