@@ -107,14 +107,21 @@ KParams make_params(hgks_solver* s, double dt, int stage) {
     kp.count_fluxes = s->count_fluxes ? 1 : 0;
     kp.report = 0;
     kp.dt = dt;
+    kp.inv_dt = dt != 0.0 ? 1.0 / dt : 0.0;
+    kp.two_mu = 2.0 * s->cfg.mu;
+    kp.rh_coef = s->cfg.mu > 0.0 ? dt / (4.0 * s->cfg.mu) : 0.0;
     kp.gas.gamma = s->cfg.gamma;
     kp.gas.gm1 = s->cfg.gamma - 1.0;
     kp.gas.K = (5.0 - 3.0 * s->cfg.gamma) / (s->cfg.gamma - 1.0);
     kp.gas.D = kp.gas.K + 3.0;
     kp.gas.mu = s->cfg.mu;
+    kp.gas.four_D = 4.0 / kp.gas.D;
     kp.dx = s->d_dx;
     kp.dy = s->d_dy;
     kp.dz = s->d_dz;
+    kp.i2dx = s->d_dx + s->nx;
+    kp.i2dy = s->d_dy + s->ny;
+    kp.i2dz = s->d_dz + (s->nzl + 2);
     kp.tab = s->d_tab;
     const auto& t = s->tabs;
     for (int a = 0; a < 3; ++a) {
@@ -353,6 +360,11 @@ int hgks_create(const hgks_config* cfg, hgks_solver** out) {
     for (int k = -1; k <= s->nzl; ++k) {
         const int kg = ((s->z0 + k) % s->nz + s->nz) % s->nz;
         dz[k + 1] = s->zs[kg + 1] - s->zs[kg];
+    }
+    // each width array is followed by its 2/h (KParams::i2dx..)
+    for (auto* v : {&dx, &dy, &dz}) {
+        const size_t n = v->size();
+        for (size_t i = 0; i < n; ++i) v->push_back(2.0 / (*v)[i]);
     }
     CK(cudaMalloc(&s->d_dx, dx.size() * sizeof(double)));
     CK(cudaMalloc(&s->d_dy, dy.size() * sizeof(double)));

@@ -6,15 +6,16 @@
 //                                 fused with the inverse mass matrix and the
 //                                 S2O4 stage combine (dg.hpp:396-449,
 //                                 solver.hpp:42-54, integrator.hpp:68-74)
-//   dt_kernel, ghost_wrap_kernel, project_kernel, tgv_kernel
 //
 // HBM layout (SoA, fp64): state q[comp][cell_g], comp = n*5 + var,
 // cell_g = i + nx*(j + ny*(k+1)) for local z layers k = -1..nzl (one ghost
 // layer each side); face buffers f_a[p*10 + (F|Ft)][i + nx*(j + ny*k)].
+// Basis/quadrature values are compile-time constants (hgks_ctables.cuh).
 #pragma once
 
 #include <stdint.h>
 
+#include "hgks_ctables.cuh"
 #include "hgks_kinetics.cuh"
 
 namespace hgks_dev {
@@ -54,12 +55,17 @@ struct KParams {
     int stage;             // 0 first residual of a step, 1 second
     int count_fluxes;
     int report;            // re-run in report mode: write err_val for the winning key
-    double dt;
+    double dt, inv_dt;
+    double two_mu;         // 2 mu: face tau = 2 mu / (p_l + p_r)
+    double rh_coef;        // dt / (4 mu): dt / (2 tau) = (p_l + p_r) rh_coef
     GasC gas;
-    const double* dx;      // [nx]
+    const double* dx;      // [nx] widths
     const double* dy;      // [ny]
     const double* dz;      // [nzl + 2] indexed k + 1
-    const double* tab;     // table image (hgks_basis.h)
+    const double* i2dx;    // 2 / h per axis (same indexing)
+    const double* i2dy;
+    const double* i2dz;
+    const double* tab;     // runtime table image (aux kernels; hgks_basis.h)
     long off_fB[3][2], off_fdB[3][2], off_fw[3];
     long off_vB, off_vdB, off_vw, off_pB, off_pdB, off_pw, off_pref, off_massf;
     unsigned long long* err_key;
@@ -87,16 +93,112 @@ __device__ __forceinline__ void report_error(const KParams& kp, unsigned long lo
 }
 
 // -------------------------------------------------------------- face kernel
+
+// Trace of one side at face point PT in the face-local frame
+// (eval_tabulated dg.hpp:139-161 + to_face_local dg.hpp:323-334).
+// SIDE 0 = minus-side cell at its plus face (ref coord +1), 1 = plus-side
+// cell at its minus face (-1). c = smem coefficients [comp][32] of the cell.
+template <int P, int DIM, int AXIS, int PT, int SIDE>
+__device__ __forceinline__ void face_trace(const double* __restrict__ c, const double* i2h,
+                                           double* t) {
+    using SH = Shape<P, DIM>;
+    constexpr int N = SH::N, NQ = SH::NQ;
+    constexpr double s = SIDE == 0 ? 1.0 : -1.0;
+    constexpr int C1 = (AXIS + 1) % 3, C2 = (AXIS + 2) % 3;
+    double e[20];
+#pragma unroll
+    for (int m = 0; m < 20; ++m) e[m] = 0.0;
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+        const double b = ctab<P, DIM>.fB[AXIS][SIDE == 0 ? 1 : 0][PT][n];
+        const double d0 = ctab<P, DIM>.fdB[AXIS][SIDE == 0 ? 1 : 0][PT][0][n];
+        const double d1 = ctab<P, DIM>.fdB[AXIS][SIDE == 0 ? 1 : 0][PT][1][n];
+        const double d2 = ctab<P, DIM>.fdB[AXIS][SIDE == 0 ? 1 : 0][PT][2][n];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+            const double cv = c[(n * 5 + v) * 32];
+            if (b != 0.0) e[v] += b * cv;
+            if (d0 != 0.0) e[5 + v] += d0 * cv;
+            if (d1 != 0.0) e[10 + v] += d1 * cv;
+            if (d2 != 0.0) e[15 + v] += d2 * cv;
+        }
+    }
+    // global -> face-local: momentum and derivative directions cycled to
+    // (AXIS, C1, C2); derivatives scaled by 2/h of their direction
+    constexpr int g[3] = {AXIS, C1, C2};
+    t[0] = e[0];
+    t[1] = e[1 + AXIS];
+    t[2] = e[1 + C1];
+    t[3] = e[1 + C2];
+    t[4] = e[4];
+#pragma unroll
+    for (int d = 1; d < 4; ++d) {
+        const int gd = g[d - 1];
+        const double* src = e + 5 + 5 * gd;
+        const double sf = i2h[gd];
+        t[5 * d + 0] = sf * src[0];
+        t[5 * d + 1] = sf * src[1 + AXIS];
+        t[5 * d + 2] = sf * src[1 + C1];
+        t[5 * d + 3] = sf * src[1 + C2];
+        t[5 * d + 4] = sf * src[4];
+    }
+}
+
+// value-only traces of both sides at PT -> pressures (for tau, dg.hpp:378-383)
+template <int P, int DIM, int AXIS, int PT>
+__device__ __forceinline__ void face_pressures(const double* __restrict__ cl,
+                                               const double* __restrict__ cr, const GasC& g,
+                                               double& pl, double& pr) {
+    using SH = Shape<P, DIM>;
+    constexpr int N = SH::N, NQ = SH::NQ;
+    double ql[5] = {0, 0, 0, 0, 0}, qr[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+        const double bl = ctab<P, DIM>.fB[AXIS][1][PT][n];
+        const double br = ctab<P, DIM>.fB[AXIS][0][PT][n];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+            ql[v] += bl * cl[(n * 5 + v) * 32];
+            qr[v] += br * cr[(n * 5 + v) * 32];
+        }
+    }
+    pl = pressure_q(ql, g);
+    pr = pressure_q(qr, g);
+}
+
+// runtime point index -> compile-time instantiation (warp-uniform branch)
+template <int P, int DIM, int AXIS, int NFP, int PT = 0>
+__device__ __forceinline__ void face_trace_rt(int p, int side, const double* c, const double* i2h,
+                                              double* t) {
+    if constexpr (PT < NFP) {
+        if (p == PT) {
+            if (side == 0) face_trace<P, DIM, AXIS, PT, 0>(c, i2h, t);
+            else face_trace<P, DIM, AXIS, PT, 1>(c, i2h, t);
+        } else {
+            face_trace_rt<P, DIM, AXIS, NFP, PT + 1>(p, side, c, i2h, t);
+        }
+    }
+}
+
+template <int P, int DIM, int AXIS, int NFP, int PT = 0>
+__device__ __forceinline__ void face_pressures_rt(int p, const double* cl, const double* cr,
+                                                  const GasC& g, double& pl, double& pr) {
+    if constexpr (PT < NFP) {
+        if (p == PT) face_pressures<P, DIM, AXIS, PT>(cl, cr, g, pl, pr);
+        else face_pressures_rt<P, DIM, AXIS, NFP, PT + 1>(p, cl, cr, g, pl, pr);
+    }
+}
+
 // CTA = 32 consecutive faces along x (one lane each) x NFP warps (one face
-// point per warp, so table reads are warp-uniform broadcasts). The two
-// neighbour cells' coefficients are staged in shared memory SoA
-// [side][comp][lane] with coalesced 256 B row loads.
+// point per warp, so the point index is warp-uniform). The two neighbour
+// cells' coefficients are staged in shared memory SoA [side][comp][lane]
+// with coalesced 256 B row loads.
 template <int P, int DIM, bool VISC, int AXIS>
 __global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>())
     face_kernel(KParams kp, const double* __restrict__ q, double* __restrict__ face,
                 int tile_x0, int tile_y0, int tile_z0) {
     using SH = Shape<P, DIM>;
-    constexpr int N = SH::N, NC = SH::NC;
+    constexpr int NC = SH::NC;
     constexpr int NFP = SH::template nfp<AXIS>();
     constexpr int NT = 32 * NFP;
     constexpr int C1 = (AXIS + 1) % 3, C2 = (AXIS + 2) % 3;
@@ -135,34 +237,24 @@ __global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>())
     const int i = i0 + lane;
     if (i >= nx) return;
 
-    // widths of the two cells
     const int im = AXIS == 0 ? (i == 0 ? nx - 1 : i - 1) : i;
     const int jm = AXIS == 1 ? (j == 0 ? ny - 1 : j - 1) : j;
     const int km = AXIS == 2 ? k - 1 : k;
-    const double hL[3] = {__ldg(kp.dx + im), __ldg(kp.dy + jm), __ldg(kp.dz + km + 1)};
-    const double hR[3] = {__ldg(kp.dx + i), __ldg(kp.dy + j), __ldg(kp.dz + k + 1)};
+    const double i2hL[3] = {__ldg(kp.i2dx + im), __ldg(kp.i2dy + jm), __ldg(kp.i2dz + km + 1)};
+    const double i2hR[3] = {__ldg(kp.i2dx + i), __ldg(kp.i2dy + j), __ldg(kp.i2dz + k + 1)};
+    const double* cL = sc + lane;
+    const double* cR = sc + NC * 32 + lane;
 
-    // left trace = minus-side cell at its plus face; right = plus-side cell at its minus face
-    const double* BL = kp.tab + kp.off_fB[AXIS][1] + p * N;
-    const double* BR = kp.tab + kp.off_fB[AXIS][0] + p * N;
-
-    // pressures of the two traces for tau = mu / mean p (dg.hpp:378-383)
-    double tau = 0.0;
+    // tau = mu / mean trace pressure (dg.hpp:378-383); dt/(2 tau) without a division
+    double tau = 0.0, rh = 0.0;
     if (VISC) {
-        double ql[5] = {0, 0, 0, 0, 0}, qr[5] = {0, 0, 0, 0, 0};
-#pragma unroll
-        for (int n = 0; n < N; ++n) {
-            const double bl = __ldg(BL + n), br = __ldg(BR + n);
-#pragma unroll
-            for (int v = 0; v < 5; ++v) {
-                ql[v] += bl * sc[(0 * NC + n * 5 + v) * 32 + lane];
-                qr[v] += br * sc[(1 * NC + n * 5 + v) * 32 + lane];
-            }
-        }
-        const double pl = pressure_q(ql, kp.gas), pr = pressure_q(qr, kp.gas);
-        tau = kp.gas.mu / (0.5 * (pl + pr));
+        double pl = 0.0, pr = 0.0;
+        face_pressures_rt<P, DIM, AXIS, NFP>(p, cL, cR, kp.gas, pl, pr);
+        const double ps = pl + pr;
+        tau = kp.two_mu / ps;
+        rh = ps * kp.rh_coef;
     }
-    const TimeW tw = time_weights(tau, kp.dt);
+    const TimeW tw = time_weights_r(tau, kp.inv_dt, rh);
 
     FluxAcc acc;
     flux_init(acc);
@@ -171,42 +263,8 @@ __global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>())
     const long item = (long)AXIS * kp.ncells_glob + f_glob;
 #pragma unroll 1
     for (int side = 0; side < 2; ++side) {
-        const double* B = side == 0 ? BL : BR;
-        const double* dB = kp.tab + kp.off_fdB[AXIS][side == 0 ? 1 : 0] + p * 3 * N;
-        const double* h = side == 0 ? hL : hR;
-        const double* c = sc + side * NC * 32 + lane;
-        double e[20];
-#pragma unroll
-        for (int m = 0; m < 20; ++m) e[m] = 0.0;
-#pragma unroll
-        for (int n = 0; n < N; ++n) {
-            const double b = __ldg(B + n);
-            const double d0 = __ldg(dB + n), d1 = __ldg(dB + N + n), d2 = __ldg(dB + 2 * N + n);
-#pragma unroll
-            for (int v = 0; v < 5; ++v) {
-                const double cv = c[(n * 5 + v) * 32];
-                e[v] += b * cv;
-                e[5 + v] += d0 * cv;
-                e[10 + v] += d1 * cv;
-                e[15 + v] += d2 * cv;
-            }
-        }
-        const double s0 = 2.0 / h[0], s1 = 2.0 / h[1], s2 = 2.0 / h[2];
-        // global -> face-local frame: momentum and derivative directions cycled
-        // to (AXIS, C1, C2) (dg.hpp:323-334)
         double t[20];
-        const double sc3[3] = {s0, s1, s2};
-#pragma unroll
-        for (int d = 0; d < 4; ++d) {
-            const int g = d == 0 ? -1 : (d == 1 ? AXIS : d == 2 ? C1 : C2);
-            const double* src = d == 0 ? e : e + 5 + 5 * g;
-            const double sf = d == 0 ? 1.0 : sc3[g < 0 ? 0 : g];
-            t[5 * d + 0] = sf * src[0];
-            t[5 * d + 1] = sf * src[1 + AXIS];
-            t[5 * d + 2] = sf * src[1 + C1];
-            t[5 * d + 3] = sf * src[1 + C2];
-            t[5 * d + 4] = sf * src[4];
-        }
+        face_trace_rt<P, DIM, AXIS, NFP>(p, side, side == 0 ? cL : cR, side == 0 ? i2hL : i2hR, t);
         double bad = 0.0;
         const int rc = flux_side<VISC>(t, side, kp.gas, tw, acc, bad);
         if (rc) {
@@ -224,19 +282,17 @@ __global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>())
     // face-local -> global (dg.hpp:336-345)
     const long fidx = (long)i + (long)nx * (j + (long)ny * k);
     double* out = face + (long)(p * 10) * kp.fs + fidx;
-    const double F[5] = {acc.F[0], acc.F[1], acc.F[2], acc.F[3], acc.F[4]};
-    const double Ft[5] = {acc.Ft[0], acc.Ft[1], acc.Ft[2], acc.Ft[3], acc.Ft[4]};
     double G[5], Gt[5];
-    G[0] = F[0];
-    G[4] = F[4];
-    G[1 + AXIS] = F[1];
-    G[1 + C1] = F[2];
-    G[1 + C2] = F[3];
-    Gt[0] = Ft[0];
-    Gt[4] = Ft[4];
-    Gt[1 + AXIS] = Ft[1];
-    Gt[1 + C1] = Ft[2];
-    Gt[1 + C2] = Ft[3];
+    G[0] = acc.F[0];
+    G[4] = acc.F[4];
+    G[1 + AXIS] = acc.F[1];
+    G[1 + C1] = acc.F[2];
+    G[1 + C2] = acc.F[3];
+    Gt[0] = acc.Ft[0];
+    Gt[4] = acc.Ft[4];
+    Gt[1 + AXIS] = acc.Ft[1];
+    Gt[1 + C1] = acc.Ft[2];
+    Gt[1 + C2] = acc.Ft[3];
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
         out[v * kp.fs] = G[v];
@@ -248,9 +304,72 @@ __global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>())
 // -------------------------------------------------------------- cell kernel
 enum : int { MODE_RESIDUAL = 0, MODE_STAGE1 = 1, MODE_STAGE2 = 2 };
 
+// value + global derivatives at volume point PT (eval_tabulated, dg.hpp:139-161)
+template <int P, int DIM, int PT, int TC>
+__device__ __forceinline__ void vol_eval(const double* __restrict__ c, const double* i2h,
+                                         double* e) {
+    using SH = Shape<P, DIM>;
+    constexpr int N = SH::N, NQ = SH::NQ;
+#pragma unroll
+    for (int m = 0; m < 20; ++m) e[m] = 0.0;
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+        const double b = ctab<P, DIM>.vB[PT][n];
+        const double d0 = ctab<P, DIM>.vdB[PT][0][n];
+        const double d1 = ctab<P, DIM>.vdB[PT][1][n];
+        const double d2 = ctab<P, DIM>.vdB[PT][2][n];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+            const double cv = c[(n * 5 + v) * TC];
+            if (b != 0.0) e[v] += b * cv;
+            if (d0 != 0.0) e[5 + v] += d0 * cv;
+            if (d1 != 0.0) e[10 + v] += d1 * cv;
+            if (d2 != 0.0) e[15 + v] += d2 * cv;
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+        e[5 + v] *= i2h[0];
+        e[10 + v] *= i2h[1];
+        e[15 + v] *= i2h[2];
+    }
+}
+
+template <int P, int DIM, int TC, int NVP, int PT = 0>
+__device__ __forceinline__ void vol_eval_rt(int p, const double* c, const double* i2h, double* e) {
+    if constexpr (PT < NVP) {
+        if (p == PT) vol_eval<P, DIM, PT, TC>(c, i2h, e);
+        else vol_eval_rt<P, DIM, TC, NVP, PT + 1>(p, c, i2h, e);
+    }
+}
+
+// face gather of one axis for one (var, F|Ft) item (dg.hpp:404-425):
+// acc[n] += sum_p w_p B-(p,n) (F-(p) - (-1)^{n_a} F+(p)), using the Legendre
+// parity B+(p,n) = (-1)^{n_a} B-(p,n).
+template <int P, int DIM, int AXIS>
+__device__ __forceinline__ void gather_axis(const double* __restrict__ fa, long fs, int row,
+                                            long fm, long fp, double* acc) {
+    using SH = Shape<P, DIM>;
+    constexpr int N = SH::N, NQ = SH::NQ;
+    constexpr int NFP = SH::template nfp<AXIS>();
+#pragma unroll
+    for (int pf = 0; pf < NFP; ++pf) {
+        const long r = (long)(pf * 10 + row) * fs;
+        const double Fm = __ldg(fa + r + fm), Fp = __ldg(fa + r + fp);
+        const double Dm = Fm - Fp, Sm = Fm + Fp;
+#pragma unroll
+        for (int n = 0; n < N; ++n) {
+            const double c = ctab<P, DIM>.fw[AXIS][pf] * ctab<P, DIM>.fB[AXIS][0][pf][n];
+            const bool odd = ctab<P, DIM>.par[AXIS][n] != 0;
+            if (c != 0.0) acc[n] += c * (odd ? Sm : Dm);
+        }
+    }
+}
+
 // CTA = TC consecutive cells along x. Phase B: one (cell, volume point) item
-// per thread -> smooth fluxes to shared memory. Phase C: one (cell, n, var)
-// item per thread -> face gather + volume projection + M^-1 + S2O4 combine.
+// per thread -> smooth fluxes to shared memory. Phase C: one (cell, var,
+// F|Ft) item per thread -> face gather + volume projection + M^-1; stage 1
+// then forms q* per coefficient, stage 2 needs only Lt2 for the combine.
 template <int P, int DIM, bool VISC, int MODE>
 __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL)
     cell_kernel(KParams kp, const double* __restrict__ qin, const double* __restrict__ f0,
@@ -260,8 +379,8 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL)
                 double* __restrict__ out1, double* __restrict__ out2, int tile_x0, int tile_y0,
                 int tile_z0) {
     using SH = Shape<P, DIM>;
-    constexpr int N = SH::N, NC = SH::NC, NVP = SH::NVP, TC = SH::TC, NT = SH::NT_CELL;
-    constexpr int NAX = SH::NAX;
+    constexpr int N = SH::N, NC = SH::NC, NQ = SH::NQ, NVP = SH::NVP, TC = SH::TC;
+    constexpr int NT = SH::NT_CELL, NAX = SH::NAX;
     extern __shared__ double smem[];
     double* sc = smem;            // [NC][TC]
     double* vf = smem + NC * TC;  // [NVP][30][TC]
@@ -281,6 +400,7 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL)
     __syncthreads();
 
     const double hy = __ldg(kp.dy + j), hz = __ldg(kp.dz + k + 1);
+    const double i2hy = __ldg(kp.i2dy + j), i2hz = __ldg(kp.i2dz + k + 1);
     const long cglob_row = (long)nx * (j + (long)ny * (k + kp.kglob0));
 
     // ---- phase B: smooth fluxes at volume points
@@ -288,32 +408,9 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL)
         const int l = it % TC, p = it / TC;
         const int i = i0 + l;
         if (i >= nx) continue;
-        const double h[3] = {__ldg(kp.dx + i), hy, hz};
-        const double* B = kp.tab + kp.off_vB + p * N;
-        const double* dB = kp.tab + kp.off_vdB + p * 3 * N;
+        const double i2h[3] = {__ldg(kp.i2dx + i), i2hy, i2hz};
         double e[20];
-#pragma unroll
-        for (int m = 0; m < 20; ++m) e[m] = 0.0;
-#pragma unroll
-        for (int n = 0; n < N; ++n) {
-            const double b = __ldg(B + n);
-            const double d0 = __ldg(dB + n), d1 = __ldg(dB + N + n), d2 = __ldg(dB + 2 * N + n);
-#pragma unroll
-            for (int v = 0; v < 5; ++v) {
-                const double cv = sc[(n * 5 + v) * TC + l];
-                e[v] += b * cv;
-                e[5 + v] += d0 * cv;
-                e[10 + v] += d1 * cv;
-                e[15 + v] += d2 * cv;
-            }
-        }
-        const double s0 = 2.0 / h[0], s1 = 2.0 / h[1], s2 = 2.0 / h[2];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-            e[5 + v] *= s0;
-            e[10 + v] *= s1;
-            e[15 + v] *= s2;
-        }
+        vol_eval_rt<P, DIM, TC, NVP>(p, sc + l, i2h, e);
         double o[30];
         double bad = 0.0;
         const int rc = smooth_flux<VISC, NAX>(e, kp.gas, o, bad);
@@ -328,74 +425,102 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL)
     if (kp.report) return;
     __syncthreads();
 
-    // ---- phase C: gather + projection + inverse mass + stage combine
-    const double* tab = kp.tab;
-    for (int it = tid; it < TC * NC; it += NT) {
-        const int l = it % TC, comp = it / TC;
-        const int n = comp / 5, v = comp - 5 * (comp / 5);
+    // ---- phase C: gather + projection + inverse mass (+ stage-2 combine)
+    // stage 2 only needs Lt2: q += dt L1 + dt^2/6 (Lt1 + 2 Lt2)
+    constexpr int FT0 = MODE == MODE_STAGE2 ? 1 : 0;
+    constexpr int NITEMS = TC * 5 * (2 - FT0);
+    const double dt = kp.dt;
+    for (int it = tid; it < NITEMS; it += NT) {
+        const int l = it % TC, vv = it / TC;
+        const int v = vv % 5, ft = FT0 + vv / 5;  // ft: 0 -> F (R), 1 -> Ft (Rt)
         const int i = i0 + l;
         if (i >= nx) continue;
-        const double h[3] = {__ldg(kp.dx + i), hy, hz};
-        double R = 0.0, Rt = 0.0;
-        // faces (dg.hpp:404-425): + w jac B- F(minus face) - w jac B+ F(plus face)
+        const double hx = __ldg(kp.dx + i);
+        const double i2h[3] = {__ldg(kp.i2dx + i), i2hy, i2hz};
+        const int row = 5 * ft + v;
+        double R[N];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const double* fa = a == 0 ? f0 : a == 1 ? f1 : f2;
-            const int nfp = a == 0 ? SH::template nfp<0>() : a == 1 ? SH::template nfp<1>()
-                                                                    : SH::template nfp<2>();
-            const double jac = h[(a + 1) % 3] * h[(a + 2) % 3] / 4.0;
-            const long fm = (long)i + (long)nx * (j + (long)ny * k);
-            long fp;
-            if (a == 0) fp = (long)(i + 1 == nx ? 0 : i + 1) + (long)nx * (j + (long)ny * k);
-            else if (a == 1) fp = (long)i + (long)nx * ((j + 1 == ny ? 0 : j + 1) + (long)ny * k);
-            else {
-                const int kp1 = (k + 1 == kp.zface_layers && kp.z_wrap) ? 0 : k + 1;
-                fp = (long)i + (long)nx * (j + (long)ny * kp1);
-            }
-            const double* Bm = tab + kp.off_fB[a][0];
-            const double* Bp = tab + kp.off_fB[a][1];
-            const double* w = tab + kp.off_fw[a];
+        for (int n = 0; n < N; ++n) R[n] = 0.0;
+        const long fm = (long)i + (long)nx * (j + (long)ny * k);
+        {
+            double acc[N];
 #pragma unroll
-            for (int pf = 0; pf < nfp; ++pf) {
-                const double wj = __ldg(w + pf) * jac;
-                const double wm = wj * __ldg(Bm + pf * N + n), wp = wj * __ldg(Bp + pf * N + n);
-                const long r0 = (long)(pf * 10 + v) * kp.fs, r1 = (long)(pf * 10 + 5 + v) * kp.fs;
-                R += wm * __ldg(fa + r0 + fm) - wp * __ldg(fa + r0 + fp);
-                Rt += wm * __ldg(fa + r1 + fm) - wp * __ldg(fa + r1 + fp);
+            for (int n = 0; n < N; ++n) acc[n] = 0.0;
+            const long fpx = (long)(i + 1 == nx ? 0 : i + 1) + (long)nx * (j + (long)ny * k);
+            gather_axis<P, DIM, 0>(f0, kp.fs, row, fm, fpx, acc);
+            const double jx = hy * hz * 0.25;  // jac = h_b h_c / 4 (dg.hpp:406)
+#pragma unroll
+            for (int n = 0; n < N; ++n) {
+                R[n] += jx * acc[n];
+                acc[n] = 0.0;
             }
+            const long fpy = (long)i + (long)nx * ((j + 1 == ny ? 0 : j + 1) + (long)ny * k);
+            gather_axis<P, DIM, 1>(f1, kp.fs, row, fm, fpy, acc);
+            const double jy = hz * hx * 0.25;
+#pragma unroll
+            for (int n = 0; n < N; ++n) {
+                R[n] += jy * acc[n];
+                acc[n] = 0.0;
+            }
+            const int kp1 = (k + 1 == kp.zface_layers && kp.z_wrap) ? 0 : k + 1;
+            const long fpz = (long)i + (long)nx * (j + (long)ny * kp1);
+            gather_axis<P, DIM, 2>(f2, kp.fs, row, fm, fpz, acc);
+            const double jz = hx * hy * 0.25;
+#pragma unroll
+            for (int n = 0; n < N; ++n) R[n] += jz * acc[n];
         }
         // volume (dg.hpp:427-448): + w (h0 h1 h2 / 8) (2/h_a) dB_a F_a
-        const double vjac = h[0] * h[1] * h[2] / 8.0;
+        const double vol = hx * hy * hz;
+        const double vjac = vol * 0.125;
 #pragma unroll
-        for (int p = 0; p < NVP; ++p) {
-            const double wj = __ldg(tab + kp.off_vw + p) * vjac;
+        for (int a = 0; a < NAX; ++a) {
+            double acc[N];
 #pragma unroll
-            for (int a = 0; a < NAX; ++a) {
-                const double wgt = wj * __ldg(tab + kp.off_vdB + (p * 3 + a) * N + n) * (2.0 / h[a]);
-                R += wgt * vf[(p * 30 + a * 10 + v) * TC + l];
-                Rt += wgt * vf[(p * 30 + a * 10 + 5 + v) * TC + l];
+            for (int n = 0; n < N; ++n) acc[n] = 0.0;
+#pragma unroll
+            for (int p = 0; p < NVP; ++p) {
+                const double F = vf[(p * 30 + a * 10 + row) * TC + l];
+#pragma unroll
+                for (int n = 0; n < N; ++n) {
+                    const double c = ctab<P, DIM>.vw[p] * ctab<P, DIM>.vdB[p][a][n];
+                    if (c != 0.0) acc[n] += c * F;
+                }
+            }
+            const double sa = vjac * i2h[a];
+#pragma unroll
+            for (int n = 0; n < N; ++n) R[n] += sa * acc[n];
+        }
+        const long g0 = (long)v * kp.cs + cbase + i;
+        if (MODE == MODE_RESIDUAL) {
+            double* o = ft ? out1 : out0;
+#pragma unroll
+            for (int n = 0; n < N; ++n) o[g0 + (long)(n * 5) * kp.cs] = R[n];
+        } else {
+            // mass_diag (dg.hpp:42-50): 1/M_n = (2nx+1)(2ny+1)(2nz+1) / vol (solver.hpp:49-51)
+            const double ivol = 1.0 / vol;
+            const double c6 = dt * dt / 6.0;
+#pragma unroll
+            for (int n = 0; n < N; ++n) {
+                const double L = R[n] * (ctab<P, DIM>.massf[n] * ivol);
+                const long gi = g0 + (long)(n * 5) * kp.cs;
+                if (MODE == MODE_STAGE1) {
+                    (ft ? out2 : out1)[gi] = L;
+                } else {
+                    out0[gi] = __ldg(qn + gi) + (dt * __ldg(L1 + gi) + c6 * (__ldg(Lt1 + gi) + 2.0 * L));
+                }
             }
         }
-        const long gi = comp * kp.cs + cbase + i;
-        if (MODE == MODE_RESIDUAL) {
-            out0[gi] = R;
-            out1[gi] = Rt;
-        } else {
-            // mass_diag (dg.hpp:42-50), inverse applied as R * (1/M) (solver.hpp:49-51)
-            const double m = h[0] * h[1] * h[2] / __ldg(tab + kp.off_massf + n);
-            const double inv = 1.0 / m;
-            const double L = R * inv, Lt = Rt * inv;
-            const double dt = kp.dt;
-            if (MODE == MODE_STAGE1) {
-                // q* = q + dt/2 L + dt^2/8 Lt (integrator.hpp:69-70)
-                out0[gi] = sc[comp * TC + l] + 0.5 * dt * L + 0.125 * dt * dt * Lt;
-                out1[gi] = L;
-                out2[gi] = Lt;
-            } else {
-                // q += dt L1 + dt^2/6 (Lt1 + 2 Lt2) (integrator.hpp:72-74)
-                const double c = dt * dt / 6.0;
-                out0[gi] = __ldg(qn + gi) + (dt * __ldg(L1 + gi) + c * (__ldg(Lt1 + gi) + 2.0 * Lt));
-            }
+    }
+    if (MODE == MODE_STAGE1) {
+        // q* = q + dt/2 L1 + dt^2/8 Lt1 (integrator.hpp:69-70) once this tile's
+        // L1 / Lt1 are written (block-scope visibility via the barrier)
+        __syncthreads();
+        for (int e = tid; e < NC * TC; e += NT) {
+            const int l = e % TC, comp = e / TC;
+            const int i = i0 + l;
+            if (i >= nx) continue;
+            const long gi = comp * kp.cs + cbase + i;
+            out0[gi] = sc[comp * TC + l] + 0.5 * dt * out1[gi] + 0.125 * dt * dt * out2[gi];
         }
     }
 }

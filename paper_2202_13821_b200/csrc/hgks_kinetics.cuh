@@ -35,11 +35,14 @@ struct GasC {
     double K;           // internal dof (core.hpp:38)
     double D;           // K + 3
     double mu;          // 1/Re (0 = Euler)
+    double four_D;      // 4 / D
 };
 
+// Maxwellian parameters; il = 1/(2 lam) = p/rho is carried so no kernel
+// divides by lam again (2 FP64 divisions per state: 1/rho and 1/p)
 struct Prim {
     double rho, U, V, W, lam;
-    double inv_rho;
+    double inv_rho, il;
 };
 
 // error codes reported through the device error key (core.hpp:58-70)
@@ -56,18 +59,19 @@ HD int prim_from_q(const double* q, const GasC& g, Prim& w, double& bad) {
         bad = q[0];
         return ERR_DENSITY;
     }
-    const double p = pressure_q(q, g);
+    const double inv = 1.0 / q[0];
+    const double p = g.gm1 * (q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) * inv);
     if (!(p > 0.0)) {
         bad = p;
         return ERR_PRESSURE;
     }
-    const double inv = 1.0 / q[0];
     w.rho = q[0];
     w.inv_rho = inv;
     w.U = q[1] * inv;
     w.V = q[2] * inv;
     w.W = q[3] * inv;
     w.lam = 0.5 * q[0] / p;
+    w.il = p * inv;  // 1/(2 lam)
     return ERR_NONE;
 }
 
@@ -83,10 +87,10 @@ HD SolveC solve_consts(const Prim& w, const GasC& g) {
     s.V = w.V;
     s.W = w.W;
     const double q2 = w.U * w.U + w.V * w.V + w.W * w.W;
-    const double sbar = 0.5 * g.D / w.lam;
+    const double sbar = g.D * w.il;  // 0.5 D / lam
     s.qs = q2 + sbar;
     s.two_lam = 2.0 * w.lam;
-    s.c5f = 4.0 * w.lam * w.lam / g.D;
+    s.c5f = (w.lam * w.lam) * g.four_D;  // 4 lam^2 / D
     return s;
 }
 
@@ -150,7 +154,7 @@ struct Tab {
 
 template <int NU, int NV>
 HD void make_tab(const Prim& w, const GasC& g, Tab<NU, NV>& t) {
-    const double il = 0.5 / w.lam;
+    const double il = w.il;
     full_seq<NU>(w.U, il, t.U);
     full_seq<NV>(w.V, il, t.V);
     full_seq<NV>(w.W, il, t.W);
@@ -237,7 +241,9 @@ struct TimeW {
     double f0F, f0Ft, anF, anFt, AnF, AnFt;  // non-equilibrium: f0, aneq, Aneq
 };
 
-HD TimeW time_weights(double tau, double dt) {
+// rh = dt / (2 tau) and inv_dt = 1/dt are passed in so callers can form them
+// without a division (the face kernel has tau = 2 mu / (p_l + p_r))
+HD TimeW time_weights_r(double tau, double inv_dt, double rh) {
     TimeW w;
     if (!(tau > 0.0)) {  // tau = 0 branch (flux.hpp:32-38)
         w.g0F = 1.0;
@@ -248,12 +254,11 @@ HD TimeW time_weights(double tau, double dt) {
         w.f0F = w.f0Ft = w.anF = w.anFt = w.AnF = w.AnFt = 0.0;
         return w;
     }
-    const double rh = 0.5 * dt / tau;
     const double s = rh > 700.0 ? 1.0 : -expm1(-rh);  // 1 - e^{-dt/(2 tau)}, clamp flux.hpp:40
-    const double x = tau / dt;
+    const double x = tau * inv_dt;
     const double t3 = s * (2.0 + s);
     const double ss = s * s;
-    const double q4 = 4.0 * x / dt;
+    const double q4 = 4.0 * x * inv_dt;
     w.g0F = 1.0 - x * t3;
     w.g0Ft = q4 * ss;
     w.f0F = x * t3;
@@ -268,6 +273,10 @@ HD TimeW time_weights(double tau, double dt) {
     w.anF = tau * (1.0 - ss) - 2.0 * tau * x * t3;
     w.anFt = -ab_t;
     return w;
+}
+
+HD TimeW time_weights(double tau, double dt) {
+    return time_weights_r(tau, 1.0 / dt, tau > 0.0 ? 0.5 * dt / tau : 0.0);
 }
 
 // Second-order BGK interface flux at one face point, already linearised in
@@ -298,7 +307,7 @@ HD int flux_side(const double* t, int side, const GasC& g, const TimeW& tw, Flux
     if (rc) return rc;
     const SolveC sc = solve_consts(w, g);
     Tab<6, 5> tb;  // U: half table (orders 0..6); V, W full
-    const double il = 0.5 / w.lam;
+    const double il = w.il;
     half_seq<6>(w.U, w.lam, il, side == 0 ? +1 : -1, tb.U);
     full_seq<5>(w.V, il, tb.V);
     full_seq<5>(w.W, il, tb.W);
@@ -357,7 +366,7 @@ HD int flux_merge(const GasC& g, const TimeW& tw, FluxAcc& acc, double& bad) {
     if (rc) return rc;
     const SolveC s0 = solve_consts(w0, g);
     Tab<6, 5> t0;
-    const double il = 0.5 / w0.lam;
+    const double il = w0.il;
     full_seq<6>(w0.U, il, t0.U);
     full_seq<5>(w0.V, il, t0.V);
     full_seq<5>(w0.W, il, t0.W);
@@ -430,7 +439,7 @@ HD int smooth_flux(const double* t, const GasC& g, double* out, double& bad) {
     Prim w;
     const int rc = prim_from_q(t, g, w, bad);
     if (rc) return rc;
-    const double tau = VISCOUS ? g.mu / (0.5 * w.rho / w.lam) : 0.0;  // tau = mu/p (dg.hpp:433)
+    const double tau = VISCOUS ? g.mu * (2.0 * w.lam * w.inv_rho) : 0.0;  // tau = mu/p (dg.hpp:433)
     const SolveC sc = solve_consts(w, g);
     Tab<6, 6> tb;
     make_tab(w, g, tb);

@@ -13,6 +13,7 @@ static GasC gas_of(double gamma, double mu) {
     g.K = (5.0 - 3.0 * gamma) / (gamma - 1.0);
     g.D = g.K + 3.0;
     g.mu = mu;
+    g.four_D = 4.0 / g.D;
     return g;
 }
 

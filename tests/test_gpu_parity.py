@@ -84,10 +84,15 @@ def test_steps_match_oracle(hgks, oracle_mod, case, n, degree, nonuni):
     q_ref = ref.get_state()[0] if hasattr(ref, "get_state") else ref.state
     q_dev, t = r.solver.get_state()
     assert rel(q_dev, q_ref) <= TOL_STATE
-    # per conserved variable as well
+    # per conserved variable as well (a variable that is identically zero in
+    # the physics, e.g. rho*W in 2-D, is rounding noise in both codes: scale it
+    # by the state magnitude instead of its own noise)
     N = r.solver.N
+    gmax = np.max(np.abs(q_ref))
     for v in range(5):
-        assert rel(q_dev.reshape(-1, N, 5)[:, :, v], q_ref.reshape(-1, N, 5)[:, :, v]) <= 1e-8
+        a, b = q_dev.reshape(-1, N, 5)[:, :, v], q_ref.reshape(-1, N, 5)[:, :, v]
+        den = max(np.max(np.abs(b)), 1e-10 * gmax)
+        assert np.max(np.abs(a - b)) / den <= 1e-8
 
 
 def test_projection_matches_oracle(hgks, oracle_mod):
