@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhgks_b200.so")
+# HGKS_LIB selects an alternate build (kernel-variant experiments only)
+LIB_PATH = os.environ.get("HGKS_LIB") or os.path.join(HERE, "libhgks_b200.so")
 
 HGKS_OK, HGKS_ERR_STATE, HGKS_ERR_CONFIG, HGKS_ERR_DT, HGKS_ERR_CUDA = 0, 1, 2, 3, 4
 

@@ -14,8 +14,10 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INC = os.path.join(os.path.dirname(HERE), "include")
-LIB = os.path.join(HERE, "libhgks_b200.so")
-OBJ = os.path.join(HERE, "_obj")
+LIB = os.environ.get("HGKS_LIB") or os.path.join(HERE, "libhgks_b200.so")
+OBJ = os.environ.get("HGKS_OBJ") or os.path.join(HERE, "_obj")
+# extra nvcc flags for kernel-variant experiments (e.g. -DHGKS_FACE_MINB=3)
+EXTRA = os.environ.get("HGKS_NVCC_EXTRA", "").split()
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -59,7 +61,7 @@ def build(force: bool = False, verbose: bool = False, log: str | None = None) ->
     def compile_unit(u):
         name, src, defs = u
         out = os.path.join(OBJ, name + ".o")
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *defs, "-I", INC, "-I", CSRC, "-dc" if False else "-c",
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *EXTRA, *defs, "-I", INC, "-I", CSRC, "-dc" if False else "-c",
                os.path.join(CSRC, src), "-o", out]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

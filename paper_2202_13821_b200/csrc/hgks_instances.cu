@@ -14,23 +14,37 @@ namespace {
 template <int P, int DIM, bool VISC>
 struct Launch {
     using SH = Shape<P, DIM>;
-    static int face_smem() { return 2 * SH::NC * 32 * (int)sizeof(double); }
+    template <int AXIS = 2>
+    static int face_smem() {
+#if HGKS_FACE_SPLIT
+        return FaceSplit<P, DIM, AXIS>::SMEM * (int)sizeof(double);
+#else
+        // staged coefficients of both neighbours + the per-thread flux accumulator
+        return (2 * SH::NC * 32 + 30 * 32 * SH::template nfp<AXIS>()) * (int)sizeof(double);
+#endif
+    }
     static int cell_smem() { return (SH::NC * SH::TC + SH::NVP * 30 * SH::TC) * (int)sizeof(double); }
 
     template <int AXIS>
     static void face_axis(const KParams& kp, const double* q, double* f, cudaStream_t st,
                           int report, const int* tile) {
-        constexpr int NFP = SH::template nfp<AXIS>();
         const int layers = AXIS == 2 ? kp.zface_layers : kp.nzl;
-        dim3 grid((kp.nx + 31) / 32, kp.ny, layers);
         int t[3] = {0, 0, 0};
         if (report) {
-            grid = dim3(1, 1, 1);
             t[0] = tile[0];
             t[1] = tile[1];
             t[2] = tile[2];
         }
-        face_kernel<P, DIM, VISC, AXIS><<<grid, 32 * NFP, face_smem(), st>>>(kp, q, f, t[0], t[1], t[2]);
+#if HGKS_FACE_SPLIT
+        using FS = FaceSplit<P, DIM, AXIS>;
+        dim3 grid(report ? FS::NGRP : ((kp.nx + 31) / 32) * FS::NGRP, report ? 1 : kp.ny,
+                  report ? 1 : layers);
+        face_kernel_split<P, DIM, VISC, AXIS><<<grid, FS::NT, face_smem<AXIS>(), st>>>(kp, q, f, t[0], t[1], t[2]);
+#else
+        constexpr int NFP = SH::template nfp<AXIS>();
+        dim3 grid(report ? 1 : (kp.nx + 31) / 32, report ? 1 : kp.ny, report ? 1 : layers);
+        face_kernel<P, DIM, VISC, AXIS><<<grid, 32 * NFP, face_smem<AXIS>(), st>>>(kp, q, f, t[0], t[1], t[2]);
+#endif
     }
     static void face(const KParams& kp, const double* q, double* const f[3], cudaStream_t st,
                      int report, const int* tile) {
@@ -67,9 +81,15 @@ struct Launch {
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         };
-        set((const void*)face_kernel<P, DIM, VISC, 0>, face_smem());
-        set((const void*)face_kernel<P, DIM, VISC, 1>, face_smem());
-        set((const void*)face_kernel<P, DIM, VISC, 2>, face_smem());
+#if HGKS_FACE_SPLIT
+        set((const void*)face_kernel_split<P, DIM, VISC, 0>, face_smem<0>());
+        set((const void*)face_kernel_split<P, DIM, VISC, 1>, face_smem<1>());
+        set((const void*)face_kernel_split<P, DIM, VISC, 2>, face_smem<2>());
+#else
+        set((const void*)face_kernel<P, DIM, VISC, 0>, face_smem<0>());
+        set((const void*)face_kernel<P, DIM, VISC, 1>, face_smem<1>());
+        set((const void*)face_kernel<P, DIM, VISC, 2>, face_smem<2>());
+#endif
         set((const void*)cell_kernel<P, DIM, VISC, MODE_RESIDUAL>, cell_smem());
         set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE1>, cell_smem());
         set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE2>, cell_smem());
@@ -79,7 +99,9 @@ struct Launch {
         KernelSet k;
         k.face = &face;
         k.cell = &cell;
-        for (int a = 0; a < 3; ++a) k.face_smem[a] = face_smem();
+        k.face_smem[0] = face_smem<0>();
+        k.face_smem[1] = face_smem<1>();
+        k.face_smem[2] = face_smem<2>();
         k.cell_smem = cell_smem();
         k.cell_tc = SH::TC;
         k.nfp[0] = SH::template nfp<0>();

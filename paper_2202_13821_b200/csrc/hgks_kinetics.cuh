@@ -216,24 +216,6 @@ HD Slope time_coefficient(const SolveC& sc, const T& t, const Slope* a) {
     return solve_unit(sc, s[0], s[1], s[2], s[3], s[4]);
 }
 
-// <u (a1 u + a2 v + a3 w) psi> (flux.hpp:59-64) accumulated with weight s
-template <class T>
-HD void directional_acc(const double* Ut, const T& t, const Slope* a, double wF, double wFt,
-                         double* F, double* Ft) {
-    double r[5], acc[5];
-    slope_moment<2, 0, 0>(Ut, t, a[0], acc);
-    slope_moment<1, 1, 0>(Ut, t, a[1], r);
-#pragma unroll
-    for (int m = 0; m < 5; ++m) acc[m] += r[m];
-    slope_moment<1, 0, 1>(Ut, t, a[2], r);
-#pragma unroll
-    for (int m = 0; m < 5; ++m) {
-        acc[m] += r[m];
-        F[m] += wF * acc[m];
-        Ft[m] += wFt * acc[m];
-    }
-}
-
 // Closed-form (F, Ft) weights of the six BGK time-coefficient terms
 // (flux.hpp:26-48 integrated over [0,dt], [0,dt/2], then flux.hpp:180-189).
 struct TimeW {
@@ -283,24 +265,67 @@ HD TimeW time_weights(double tau, double dt) {
 // time: F and dF/dt at t_n (flux.hpp:71-124 + :180-189), split into one pass
 // per side plus a merge so a kernel can build each trace just in time.
 // Traces are in the face-local frame: q[5], dq_n[5], dq_t1[5], dq_t2[5].
+// The 30-double accumulator that lives across the passes is reached through
+// an accessor: registers (FluxAcc) or a per-thread shared-memory column
+// (SmemAcc, frees ~60 registers in the face kernel).
 struct FluxAcc {
-    double q0[5];      // rho_l <psi>_+ + rho_r <psi>_-        (flux.hpp:85-86)
-    double dq0[3][5];  // rho_l <a_l psi>_+ + rho_r <a_r psi>_- (flux.hpp:92-93)
-    double F[5], Ft[5];
+    double q0_[5];      // rho_l <psi>_+ + rho_r <psi>_-        (flux.hpp:85-86)
+    double dq0_[3][5];  // rho_l <a_l psi>_+ + rho_r <a_r psi>_- (flux.hpp:92-93)
+    double F_[5], Ft_[5];
+    HD double& q0(int m) { return q0_[m]; }
+    HD double& dq0(int d, int m) { return dq0_[d][m]; }
+    HD double& F(int m) { return F_[m]; }
+    HD double& Ft(int m) { return Ft_[m]; }
 };
 
-HD void flux_init(FluxAcc& acc) {
+// [slot][thread] layout: consecutive lanes hit consecutive 8-byte words
+struct SmemAcc {
+    double* p;   // &base[tid]
+    int stride;  // threads per CTA
+    HD double& q0(int m) { return p[m * stride]; }
+    HD double& dq0(int d, int m) { return p[(5 + 5 * d + m) * stride]; }
+    HD double& F(int m) { return p[(20 + m) * stride]; }
+    HD double& Ft(int m) { return p[(25 + m) * stride]; }
+};
+
+template <class Acc>
+HD void flux_init(Acc& acc) {
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
-        acc.q0[m] = 0.0;
-        acc.dq0[0][m] = acc.dq0[1][m] = acc.dq0[2][m] = 0.0;
-        acc.F[m] = acc.Ft[m] = 0.0;
+        acc.q0(m) = 0.0;
+        acc.dq0(0, m) = 0.0;
+        acc.dq0(1, m) = 0.0;
+        acc.dq0(2, m) = 0.0;
+        acc.F(m) = 0.0;
+        acc.Ft(m) = 0.0;
     }
 }
 
+template <class Acc>
+HD void acc_flux(Acc& acc, double sF, double sFt, const double* r) {
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+        acc.F(m) += sF * r[m];
+        acc.Ft(m) += sFt * r[m];
+    }
+}
+
+// <u (a1 u + a2 v + a3 w) psi> (flux.hpp:59-64)
+template <class T>
+HD void directional_flux(const double* Ut, const T& t, const Slope* a, double* out) {
+    double r[5];
+    slope_moment<2, 0, 0>(Ut, t, a[0], out);
+    slope_moment<1, 1, 0>(Ut, t, a[1], r);
+#pragma unroll
+    for (int m = 0; m < 5; ++m) out[m] += r[m];
+    slope_moment<1, 0, 1>(Ut, t, a[2], r);
+#pragma unroll
+    for (int m = 0; m < 5; ++m) out[m] += r[m];
+}
+
 // side 0 = left (u>0 half), 1 = right (u<0 half). Returns ERR_*.
-template <bool VISCOUS>
-HD int flux_side(const double* t, int side, const GasC& g, const TimeW& tw, FluxAcc& acc,
+template <bool VISCOUS, class Acc>
+HD int flux_side(const double* t, int side, const GasC& g, const TimeW& tw, Acc& acc,
                  double& bad) {
     Prim w;
     const int rc = prim_from_q(t, g, w, bad);
@@ -319,12 +344,12 @@ HD int flux_side(const double* t, int side, const GasC& g, const TimeW& tw, Flux
     double r[5];
     psi_moment<0, 0, 0>(tb.U, tb, r);
 #pragma unroll
-    for (int m = 0; m < 5; ++m) acc.q0[m] += w.rho * r[m];
+    for (int m = 0; m < 5; ++m) acc.q0(m) += w.rho * r[m];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
         slope_moment<0, 0, 0>(tb.U, tb, a[d], r);
 #pragma unroll
-        for (int m = 0; m < 5; ++m) acc.dq0[d][m] += w.rho * r[m];
+        for (int m = 0; m < 5; ++m) acc.dq0(d, m) += w.rho * r[m];
     }
     if (VISCOUS) {
         // A from compatibility with the full table (flux.hpp:109-110)
@@ -340,29 +365,23 @@ HD int flux_side(const double* t, int side, const GasC& g, const TimeW& tw, Flux
         const Slope A = time_coefficient(sc, tf, a);
         // free-streaming terms of this side (flux.hpp:112-121)
         psi_moment<1, 0, 0>(tb.U, tb, r);
-        const double sF0 = w.rho * tw.f0F, sFt0 = w.rho * tw.f0Ft;
-#pragma unroll
-        for (int m = 0; m < 5; ++m) {
-            acc.F[m] += sF0 * r[m];
-            acc.Ft[m] += sFt0 * r[m];
-        }
-        directional_acc(tb.U, tb, a, w.rho * tw.anF, w.rho * tw.anFt, acc.F, acc.Ft);
+        acc_flux(acc, w.rho * tw.f0F, w.rho * tw.f0Ft, r);
+        directional_flux(tb.U, tb, a, r);
+        acc_flux(acc, w.rho * tw.anF, w.rho * tw.anFt, r);
         slope_moment<1, 0, 0>(tb.U, tb, A, r);
-        const double sF1 = w.rho * tw.AnF, sFt1 = w.rho * tw.AnFt;
-#pragma unroll
-        for (int m = 0; m < 5; ++m) {
-            acc.F[m] += sF1 * r[m];
-            acc.Ft[m] += sFt1 * r[m];
-        }
+        acc_flux(acc, w.rho * tw.AnF, w.rho * tw.AnFt, r);
     }
     return ERR_NONE;
 }
 
 // equilibrium part from the merged state (flux.hpp:87-106); F/Ft final after.
-template <bool VISCOUS>
-HD int flux_merge(const GasC& g, const TimeW& tw, FluxAcc& acc, double& bad) {
+template <bool VISCOUS, class Acc>
+HD int flux_merge(const GasC& g, const TimeW& tw, Acc& acc, double& bad) {
     Prim w0;
-    const int rc = prim_from_q(acc.q0, g, w0, bad);
+    double q0[5];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) q0[m] = acc.q0(m);
+    const int rc = prim_from_q(q0, g, w0, bad);
     if (rc) return rc;
     const SolveC s0 = solve_consts(w0, g);
     Tab<6, 5> t0;
@@ -374,30 +393,86 @@ HD int flux_merge(const GasC& g, const TimeW& tw, FluxAcc& acc, double& bad) {
     t0.dxi = 2.0 * g.K * il * il;
     Slope ab[3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) ab[d] = micro_slope(s0, w0.inv_rho, acc.dq0[d]);
+    for (int d = 0; d < 3; ++d) {
+        double dq[5];
+#pragma unroll
+        for (int m = 0; m < 5; ++m) dq[m] = acc.dq0(d, m);
+        ab[d] = micro_slope(s0, w0.inv_rho, dq);
+    }
     const Slope Ab = time_coefficient(s0, t0, ab);
     double r[5];
     psi_moment<1, 0, 0>(t0.U, t0, r);
-    {
-        const double sF = w0.rho * tw.g0F, sFt = w0.rho * tw.g0Ft;
-#pragma unroll
-        for (int m = 0; m < 5; ++m) {
-            acc.F[m] += sF * r[m];
-            acc.Ft[m] += sFt * r[m];
-        }
-    }
+    acc_flux(acc, w0.rho * tw.g0F, w0.rho * tw.g0Ft, r);
     // abar's weight vanishes at tau = 0 (flux.hpp:32-37)
-    if (VISCOUS) directional_acc(t0.U, t0, ab, w0.rho * tw.abF, w0.rho * tw.abFt, acc.F, acc.Ft);
+    if (VISCOUS) {
+        directional_flux(t0.U, t0, ab, r);
+        acc_flux(acc, w0.rho * tw.abF, w0.rho * tw.abFt, r);
+    }
     slope_moment<1, 0, 0>(t0.U, t0, Ab, r);
-    {
-        const double sF = w0.rho * tw.AbF, sFt = w0.rho * tw.AbFt;
+    acc_flux(acc, w0.rho * tw.AbF, w0.rho * tw.AbFt, r);
+    return ERR_NONE;
+}
+
+// The merge split in two halves for two cooperating threads: both build the
+// merged state (setup), then part A adds g0 + Abar terms (time coefficient +
+// 2 moments) and part B the abar term (3 slope moments); the halves' F/Ft
+// sum to flux_merge's.
+struct MergeState {
+    Prim w0;
+    SolveC s0;
+    Tab<6, 5> t0;
+    Slope ab[3];
+};
+
+HD int merge_setup(const GasC& g, const double* q0, const double* dq0 /*[3][5]*/, MergeState& M,
+                   double& bad) {
+    const int rc = prim_from_q(q0, g, M.w0, bad);
+    if (rc) return rc;
+    M.s0 = solve_consts(M.w0, g);
+    const double il = M.w0.il;
+    full_seq<6>(M.w0.U, il, M.t0.U);
+    full_seq<5>(M.w0.V, il, M.t0.V);
+    full_seq<5>(M.w0.W, il, M.t0.W);
+    M.t0.xi2 = g.K * il;
+    M.t0.dxi = 2.0 * g.K * il * il;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) M.ab[d] = micro_slope(M.s0, M.w0.inv_rho, dq0 + 5 * d);
+    return ERR_NONE;
+}
+
+HD void merge_part_a(const MergeState& M, const TimeW& tw, double* F, double* Ft) {
+    const Slope Ab = time_coefficient(M.s0, M.t0, M.ab);
+    double r[5];
+    psi_moment<1, 0, 0>(M.t0.U, M.t0, r);
+    const double sF = M.w0.rho * tw.g0F, sFt = M.w0.rho * tw.g0Ft;
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+        F[m] = sF * r[m];
+        Ft[m] = sFt * r[m];
+    }
+    slope_moment<1, 0, 0>(M.t0.U, M.t0, Ab, r);
+    const double aF = M.w0.rho * tw.AbF, aFt = M.w0.rho * tw.AbFt;
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+        F[m] += aF * r[m];
+        Ft[m] += aFt * r[m];
+    }
+}
+
+template <bool VISCOUS>
+HD void merge_part_b(const MergeState& M, const TimeW& tw, double* F, double* Ft) {
+#pragma unroll
+    for (int m = 0; m < 5; ++m) F[m] = Ft[m] = 0.0;
+    if (VISCOUS) {  // abar's weight vanishes at tau = 0 (flux.hpp:32-37)
+        double r[5];
+        directional_flux(M.t0.U, M.t0, M.ab, r);
+        const double sF = M.w0.rho * tw.abF, sFt = M.w0.rho * tw.abFt;
 #pragma unroll
         for (int m = 0; m < 5; ++m) {
-            acc.F[m] += sF * r[m];
-            acc.Ft[m] += sFt * r[m];
+            F[m] = sF * r[m];
+            Ft[m] = sFt * r[m];
         }
     }
-    return ERR_NONE;
 }
 
 // Whole interface flux from two traces; stage = 0 left, 1 right, 2 merged on
@@ -424,8 +499,8 @@ HD int interface_flux(const double* tl, const double* tr, const GasC& g, const T
     }
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
-        F[m] = acc.F[m];
-        Ft[m] = acc.Ft[m];
+        F[m] = acc.F(m);
+        Ft[m] = acc.Ft(m);
     }
     return ERR_NONE;
 }
