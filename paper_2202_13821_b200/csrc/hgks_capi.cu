@@ -344,9 +344,9 @@ int hgks_create(const hgks_config* cfg, hgks_solver** out) {
     s->zface_layers = s->single ? s->nzl : s->nzl + 1;
     s->fs = ((s->S * s->zface_layers + pad - 1) / pad) * pad;
     cudaError_t ce;
-    if (!pick_kernels(cfg->degree, cfg->dim, cfg->mu > 0.0, s->ks, ce)) return bad("no kernels for this degree/dim");
     *out = s;
-    CK(cudaSetDevice(cfg->device));
+    CK(cudaSetDevice(cfg->device));  // kernel attributes / occupancy below are per device
+    if (!pick_kernels(cfg->degree, cfg->dim, cfg->mu > 0.0, s->ks, ce)) return bad("no kernels for this degree/dim");
     if (ce != cudaSuccess) return cuda_fail(s, ce, "cudaFuncSetAttribute");
     CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     s->own_stream = true;

@@ -1,6 +1,8 @@
 // Explicit kernel instantiation unit: one translation unit per
 // (degree, dim) family (HGKS_INST_P, HGKS_INST_DIM), compiled in parallel by
 // build.py. Each exports pick_<P>_<DIM>() for the dispatcher in hgks_capi.cu.
+#include <algorithm>
+
 #include "hgks_launch.h"
 
 #ifndef HGKS_INST_P
@@ -23,7 +25,9 @@ struct Launch {
         return (2 * SH::NC * 32 + 30 * 32 * SH::template nfp<AXIS>()) * (int)sizeof(double);
 #endif
     }
-    static int cell_smem() { return (SH::NC * SH::TC + SH::NVP * 30 * SH::TC) * (int)sizeof(double); }
+    static int cell_smem() { return CellTile<P, DIM>::SMEM * (int)sizeof(double); }
+    // persistent cell kernel: resident CTAs on the whole GPU (set by configure)
+    static inline int cell_grid[3] = {0, 0, 0};
 
     template <int AXIS>
     static void face_axis(const KParams& kp, const double* q, double* f, cudaStream_t st,
@@ -56,24 +60,25 @@ struct Launch {
     static void cell(const KParams& kp, int mode, const double* qin, double* const f[3],
                      const double* qn, const double* L1, const double* Lt1, double* o0, double* o1,
                      double* o2, cudaStream_t st, int report, const int* tile) {
-        dim3 grid((kp.nx + SH::TC - 1) / SH::TC, kp.ny, kp.nzl);
-        int t[3] = {0, 0, 0};
-        if (report) {
-            grid = dim3(1, 1, 1);
-            t[0] = tile[0];
-            t[1] = tile[1];
-            t[2] = tile[2];
+        const int ntx = (kp.nx + SH::TC - 1) / SH::TC;
+        const int ntiles = ntx * kp.ny * kp.nzl;
+        int first = 0, count = ntiles;
+        int grid = std::min(ntiles, std::max(1, cell_grid[mode]));
+        if (report) {  // the failing cell's tile only
+            first = tile[0] + ntx * (tile[1] + kp.ny * tile[2]);
+            count = 1;
+            grid = 1;
         }
         const int smem = cell_smem();
         if (mode == MODE_RESIDUAL)
             cell_kernel<P, DIM, VISC, MODE_RESIDUAL><<<grid, SH::NT_CELL, smem, st>>>(
-                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, t[0], t[1], t[2]);
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
         else if (mode == MODE_STAGE1)
             cell_kernel<P, DIM, VISC, MODE_STAGE1><<<grid, SH::NT_CELL, smem, st>>>(
-                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, t[0], t[1], t[2]);
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
         else
             cell_kernel<P, DIM, VISC, MODE_STAGE2><<<grid, SH::NT_CELL, smem, st>>>(
-                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, t[0], t[1], t[2]);
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
     }
     static cudaError_t configure() {
         cudaError_t e = cudaSuccess;
@@ -93,6 +98,18 @@ struct Launch {
         set((const void*)cell_kernel<P, DIM, VISC, MODE_RESIDUAL>, cell_smem());
         set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE1>, cell_smem());
         set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE2>, cell_smem());
+        if (e != cudaSuccess) return e;
+        int dev = 0, sms = 0;
+        e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const void* fns[3] = {(const void*)cell_kernel<P, DIM, VISC, MODE_RESIDUAL>,
+                              (const void*)cell_kernel<P, DIM, VISC, MODE_STAGE1>,
+                              (const void*)cell_kernel<P, DIM, VISC, MODE_STAGE2>};
+        for (int m = 0; m < 3 && e == cudaSuccess; ++m) {
+            int nb = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fns[m], SH::NT_CELL, cell_smem());
+            cell_grid[m] = std::max(1, nb) * sms;
+        }
         return e;
     }
     static KernelSet set() {

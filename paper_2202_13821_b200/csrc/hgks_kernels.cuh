@@ -31,6 +31,10 @@
 #endif
 // P3 face CTAs have 9 warps: one CTA per SM keeps them spill-free
 #define HGKS_FACE_MINB_P(P) ((P) == 3 ? 1 : HGKS_FACE_MINB)
+// cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
+#ifndef HGKS_CELL_TC
+#define HGKS_CELL_TC 16
+#endif
 
 namespace hgks_dev {
 
@@ -52,9 +56,11 @@ struct Shape {
         return DIM == 3 ? NQ * NQ : (AXIS == 2 ? NQ * NQ : NQ);
     }
     static constexpr int NAX = DIM == 3 ? 3 : 2;
-    // cell tile along x and threads of the cell kernel
-    static constexpr int TC = P == 3 ? 8 : 32;
-    static constexpr int NT_CELL = P == 3 ? 224 : 256;
+    // cell tile along x and threads of the cell kernel (one thread per
+    // (cell, volume point) in phase B for P1/P2)
+    static constexpr int TC = P == 3 ? 8 : HGKS_CELL_TC;
+    static constexpr int NT_CELL = P == 3 ? 224 : HGKS_CELL_TC * NVP;
+    static constexpr int MINB_CELL = P == 3 ? 1 : (HGKS_CELL_TC <= 16 ? 2 : 1);
 };
 
 struct KParams {
@@ -505,186 +511,258 @@ __device__ __forceinline__ void vol_eval_rt(int p, const double* c, const double
     }
 }
 
-// face gather of one axis for one (var, F|Ft) item (dg.hpp:404-425):
-// acc[n] += sum_p w_p B-(p,n) (F-(p) - (-1)^{n_a} F+(p)), using the Legendre
-// parity B+(p,n) = (-1)^{n_a} B-(p,n).
-template <int P, int DIM, int AXIS>
-__device__ __forceinline__ void gather_axis(const double* __restrict__ fa, long fs, int row,
-                                            long fm, long fp, double* acc) {
-    using SH = Shape<P, DIM>;
-    constexpr int N = SH::N, NQ = SH::NQ;
-    constexpr int NFP = SH::template nfp<AXIS>();
-#pragma unroll
-    for (int pf = 0; pf < NFP; ++pf) {
-        const long r = (long)(pf * 10 + row) * fs;
-        const double Fm = __ldg(fa + r + fm), Fp = __ldg(fa + r + fp);
-        const double Dm = Fm - Fp, Sm = Fm + Fp;
-#pragma unroll
-        for (int n = 0; n < N; ++n) {
-            const double c = ctab<P, DIM>.fw[AXIS][pf] * ctab<P, DIM>.fB[AXIS][0][pf][n];
-            const bool odd = ctab<P, DIM>.par[AXIS][n] != 0;
-            if (c != 0.0) acc[n] += c * (odd ? Sm : Dm);
-        }
-    }
+// async global->shared copies (cp.async, LDGSTS): the persistent kernels
+// prefetch the next tile while computing the current one
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+                 "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// CTA = TC consecutive cells along x. Phase B: one (cell, volume point) item
-// per thread -> smooth fluxes to shared memory. Phase C: one (cell, var,
-// F|Ft) item per thread -> face gather + volume projection + M^-1; stage 1
-// then forms q* per coefficient, stage 2 needs only Lt2 for the combine.
+// shared-memory plan of one cell-kernel CTA (doubles)
+template <int P, int DIM>
+struct CellTile {
+    using SH = Shape<P, DIM>;
+    static constexpr int TC = SH::TC, NC = SH::NC, NVP = SH::NVP;
+    static constexpr int NFX = SH::template nfp<0>(), NFY = SH::template nfp<1>(),
+                         NFZ = SH::template nfp<2>();
+    static constexpr int COEF = NC * TC;           // one coefficient tile [NC][TC]
+    static constexpr int FX = NFX * 10 * (TC + 1); // x faces i0..i0+TC   [pf*10+c][TC+1]
+    static constexpr int FY = NFY * 10 * 2 * TC;   // y faces rows j, j+1 [pf*10+c][2][TC]
+    static constexpr int FZ = NFZ * 10 * 2 * TC;   // z faces layers k, k+1
+    static constexpr int VF = NVP * 30 * TC;       // volume-point fluxes [p][30][TC]
+    static constexpr int LB = 2 * NC * TC;         // L, Lt of the tile (stage-1 q*)
+    static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + LB;
+};
+
+// Persistent CTA over tiles of TC consecutive cells along x, software
+// pipelined: while tile t is computed, the coefficients of tile t+grid and
+// the face fluxes of tile t stream into shared memory (cp.async).
+// Phase B: one (cell, volume point) item per thread -> smooth fluxes.
+// Phase C: one (cell, var, F|Ft) item per thread -> face gather + volume
+// projection + M^-1 (+ S2O4 combine); stage 1 then forms q* per coefficient
+// from shared memory, stage 2 needs only Lt2.
 template <int P, int DIM, bool VISC, int MODE>
-__global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL)
+__global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CELL)
     cell_kernel(KParams kp, const double* __restrict__ qin, const double* __restrict__ f0,
                 const double* __restrict__ f1, const double* __restrict__ f2,
                 const double* __restrict__ qn, const double* __restrict__ L1,
                 const double* __restrict__ Lt1, double* __restrict__ out0,
-                double* __restrict__ out1, double* __restrict__ out2, int tile_x0, int tile_y0,
-                int tile_z0) {
+                double* __restrict__ out1, double* __restrict__ out2, int tile_first,
+                int tile_count, int unused) {
     using SH = Shape<P, DIM>;
-    constexpr int N = SH::N, NC = SH::NC, NQ = SH::NQ, NVP = SH::NVP, TC = SH::TC;
+    using CT = CellTile<P, DIM>;
+    constexpr int N = SH::N, NC = SH::NC, NVP = SH::NVP, TC = SH::TC;
     constexpr int NT = SH::NT_CELL, NAX = SH::NAX;
     extern __shared__ double smem[];
-    double* sc = smem;            // [NC][TC]
-    double* vf = smem + NC * TC;  // [NVP][30][TC]
+    double* coefb = smem;                 // [2][NC][TC]
+    double* fx = coefb + 2 * CT::COEF;
+    double* fy = fx + CT::FX;
+    double* fz = fy + CT::FY;
+    double* vf = fz + CT::FZ;             // [NVP][30][TC]
+    double* lb = vf + CT::VF;             // [2][NC][TC]
 
     const int tid = threadIdx.x;
-    const int i0 = (blockIdx.x + tile_x0) * TC;
-    const int j = blockIdx.y + tile_y0;
-    const int k = blockIdx.z + tile_z0;
     const int nx = kp.nx, ny = kp.ny;
-    const long cbase = (long)(k + 1) * kp.S + (long)j * nx;
+    const int ntx = (nx + TC - 1) / TC;
+    const int tile_end = tile_first + tile_count;
+    const int step = kp.report ? tile_count : gridDim.x;
 
-    for (int e = tid; e < NC * TC; e += NT) {
-        const int l = e % TC, comp = e / TC;
-        const int i = i0 + l;
-        sc[comp * TC + l] = i < nx ? __ldg(qin + comp * kp.cs + cbase + i) : 0.0;
-    }
-    __syncthreads();
-
-    const double hy = __ldg(kp.dy + j), hz = __ldg(kp.dz + k + 1);
-    const double i2hy = __ldg(kp.i2dy + j), i2hz = __ldg(kp.i2dz + k + 1);
-    const long cglob_row = (long)nx * (j + (long)ny * (k + kp.kglob0));
-
-    // ---- phase B: smooth fluxes at volume points
-    for (int it = tid; it < TC * NVP; it += NT) {
-        const int l = it % TC, p = it / TC;
-        const int i = i0 + l;
-        if (i >= nx) continue;
-        const double i2h[3] = {__ldg(kp.i2dx + i), i2hy, i2hz};
-        double e[20];
-        vol_eval_rt<P, DIM, TC, NVP>(p, sc + l, i2h, e);
-        double o[30];
-        double bad = 0.0;
-        const int rc = smooth_flux<VISC, NAX>(e, kp.gas, o, bad);
-        if (rc) {
-            report_error(kp, err_key(kp.stage, 1, cglob_row + i, p, 0, rc), bad);
-#pragma unroll
-            for (int m = 0; m < 30; ++m) o[m] = 0.0;
-        }
-#pragma unroll
-        for (int m = 0; m < 10 * NAX; ++m) vf[(p * 30 + m) * TC + l] = o[m];
-    }
-    if (kp.report) return;
-    __syncthreads();
-
-    // ---- phase C: gather + projection + inverse mass (+ stage-2 combine)
-    // stage 2 only needs Lt2: q += dt L1 + dt^2/6 (Lt1 + 2 Lt2)
-    constexpr int FT0 = MODE == MODE_STAGE2 ? 1 : 0;
-    constexpr int NITEMS = TC * 5 * (2 - FT0);
-    const double dt = kp.dt;
-    for (int it = tid; it < NITEMS; it += NT) {
-        const int l = it % TC, vv = it / TC;
-        const int v = vv % 5, ft = FT0 + vv / 5;  // ft: 0 -> F (R), 1 -> Ft (Rt)
-        const int i = i0 + l;
-        if (i >= nx) continue;
-        const double hx = __ldg(kp.dx + i);
-        const double i2h[3] = {__ldg(kp.i2dx + i), i2hy, i2hz};
-        const int row = 5 * ft + v;
-        double R[N];
-#pragma unroll
-        for (int n = 0; n < N; ++n) R[n] = 0.0;
-        const long fm = (long)i + (long)nx * (j + (long)ny * k);
-        {
-            double acc[N];
-#pragma unroll
-            for (int n = 0; n < N; ++n) acc[n] = 0.0;
-            const long fpx = (long)(i + 1 == nx ? 0 : i + 1) + (long)nx * (j + (long)ny * k);
-            gather_axis<P, DIM, 0>(f0, kp.fs, row, fm, fpx, acc);
-            const double jx = hy * hz * 0.25;  // jac = h_b h_c / 4 (dg.hpp:406)
-#pragma unroll
-            for (int n = 0; n < N; ++n) {
-                R[n] += jx * acc[n];
-                acc[n] = 0.0;
-            }
-            const long fpy = (long)i + (long)nx * ((j + 1 == ny ? 0 : j + 1) + (long)ny * k);
-            gather_axis<P, DIM, 1>(f1, kp.fs, row, fm, fpy, acc);
-            const double jy = hz * hx * 0.25;
-#pragma unroll
-            for (int n = 0; n < N; ++n) {
-                R[n] += jy * acc[n];
-                acc[n] = 0.0;
-            }
-            const int kp1 = (k + 1 == kp.zface_layers && kp.z_wrap) ? 0 : k + 1;
-            const long fpz = (long)i + (long)nx * (j + (long)ny * kp1);
-            gather_axis<P, DIM, 2>(f2, kp.fs, row, fm, fpz, acc);
-            const double jz = hx * hy * 0.25;
-#pragma unroll
-            for (int n = 0; n < N; ++n) R[n] += jz * acc[n];
-        }
-        // volume (dg.hpp:427-448): + w (h0 h1 h2 / 8) (2/h_a) dB_a F_a
-        const double vol = hx * hy * hz;
-        const double vjac = vol * 0.125;
-#pragma unroll
-        for (int a = 0; a < NAX; ++a) {
-            double acc[N];
-#pragma unroll
-            for (int n = 0; n < N; ++n) acc[n] = 0.0;
-#pragma unroll
-            for (int p = 0; p < NVP; ++p) {
-                const double F = vf[(p * 30 + a * 10 + row) * TC + l];
-#pragma unroll
-                for (int n = 0; n < N; ++n) {
-                    const double c = ctab<P, DIM>.vw[p] * ctab<P, DIM>.vdB[p][a][n];
-                    if (c != 0.0) acc[n] += c * F;
-                }
-            }
-            const double sa = vjac * i2h[a];
-#pragma unroll
-            for (int n = 0; n < N; ++n) R[n] += sa * acc[n];
-        }
-        const long g0 = (long)v * kp.cs + cbase + i;
-        if (MODE == MODE_RESIDUAL) {
-            double* o = ft ? out1 : out0;
-#pragma unroll
-            for (int n = 0; n < N; ++n) o[g0 + (long)(n * 5) * kp.cs] = R[n];
-        } else {
-            // mass_diag (dg.hpp:42-50): 1/M_n = (2nx+1)(2ny+1)(2nz+1) / vol (solver.hpp:49-51)
-            const double ivol = 1.0 / vol;
-            const double c6 = dt * dt / 6.0;
-#pragma unroll
-            for (int n = 0; n < N; ++n) {
-                const double L = R[n] * (ctab<P, DIM>.massf[n] * ivol);
-                const long gi = g0 + (long)(n * 5) * kp.cs;
-                if (MODE == MODE_STAGE1) {
-                    (ft ? out2 : out1)[gi] = L;
-                } else {
-                    out0[gi] = __ldg(qn + gi) + (dt * __ldg(L1 + gi) + c6 * (__ldg(Lt1 + gi) + 2.0 * L));
-                }
-            }
-        }
-    }
-    if (MODE == MODE_STAGE1) {
-        // q* = q + dt/2 L1 + dt^2/8 Lt1 (integrator.hpp:69-70) once this tile's
-        // L1 / Lt1 are written (block-scope visibility via the barrier)
-        __syncthreads();
-        for (int e = tid; e < NC * TC; e += NT) {
+    auto tile_ijk = [&](int t, int& i0, int& j, int& k) {
+        i0 = (t % ntx) * TC;
+        j = (t / ntx) % ny;
+        k = t / (ntx * ny);
+    };
+    auto prefetch_coef = [&](int t, double* dst) {
+        int i0, j, k;
+        tile_ijk(t, i0, j, k);
+        const long cbase = (long)(k + 1) * kp.S + (long)j * nx;
+        for (int e = tid; e < CT::COEF; e += NT) {
             const int l = e % TC, comp = e / TC;
+            const bool ok = i0 + l < nx;
+            cp_async8(dst + comp * TC + l, qin + comp * kp.cs + cbase + (ok ? i0 + l : 0), ok);
+        }
+    };
+    auto prefetch_faces = [&](int t) {
+        int i0, j, k;
+        tile_ijk(t, i0, j, k);
+        const long rowk = (long)nx * (j + (long)ny * k);
+        for (int e = tid; e < CT::FX; e += NT) {  // x faces i0 .. i0+TC (periodic wrap at nx)
+            const int l = e % (TC + 1), r = e / (TC + 1);
+            const int ig = i0 + l;
+            const bool ok = ig <= nx;  // x is always periodic: face nx is face 0
+            const int iw = ig == nx ? 0 : ig;
+            cp_async8(fx + e, f0 + (long)r * kp.fs + rowk + (ok ? iw : 0), ok);
+        }
+        const int jp = j + 1 == ny ? 0 : j + 1;
+        const long rowp = (long)nx * (jp + (long)ny * k);
+        for (int e = tid; e < CT::FY; e += NT) {  // y faces of rows j, j+1
+            const int l = e % (2 * TC), r = e / (2 * TC);
+            const int ig = i0 + (l % TC);
+            const bool ok = ig < nx;
+            cp_async8(fy + e, f1 + (long)r * kp.fs + (l < TC ? rowk : rowp) + (ok ? ig : 0), ok);
+        }
+        const int kp1 = (k + 1 == kp.zface_layers && kp.z_wrap) ? 0 : k + 1;
+        const long rowz = (long)nx * (j + (long)ny * kp1);
+        for (int e = tid; e < CT::FZ; e += NT) {  // z faces of layers k, k+1
+            const int l = e % (2 * TC), r = e / (2 * TC);
+            const int ig = i0 + (l % TC);
+            const bool ok = ig < nx;
+            cp_async8(fz + e, f2 + (long)r * kp.fs + (l < TC ? rowk : rowz) + (ok ? ig : 0), ok);
+        }
+    };
+
+    const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
+    if (t0 < tile_end) prefetch_coef(t0, coefb);
+    cp_async_commit();
+    const double dt = kp.dt;
+    int n = 0;
+    for (int t = t0; t < tile_end; t += step, ++n) {
+        double* sc = coefb + (n & 1) * CT::COEF;
+        prefetch_faces(t);
+        cp_async_commit();
+        if (t + step < tile_end) prefetch_coef(t + step, coefb + ((n + 1) & 1) * CT::COEF);
+        cp_async_commit();
+        int i0, j, k;
+        tile_ijk(t, i0, j, k);
+        const long cbase = (long)(k + 1) * kp.S + (long)j * nx;
+        const double hy = __ldg(kp.dy + j), hz = __ldg(kp.dz + k + 1);
+        const double i2hy = __ldg(kp.i2dy + j), i2hz = __ldg(kp.i2dz + k + 1);
+        const long cglob_row = (long)nx * (j + (long)ny * (k + kp.kglob0));
+        cp_async_wait<2>();  // this tile's coefficients
+        __syncthreads();
+
+        // ---- phase B: smooth fluxes at volume points
+        for (int it = tid; it < TC * NVP; it += NT) {
+            const int l = it % TC, p = it / TC;
             const int i = i0 + l;
             if (i >= nx) continue;
-            const long gi = comp * kp.cs + cbase + i;
-            out0[gi] = sc[comp * TC + l] + 0.5 * dt * out1[gi] + 0.125 * dt * dt * out2[gi];
+            const double i2h[3] = {__ldg(kp.i2dx + i), i2hy, i2hz};
+            double e[20];
+            vol_eval_rt<P, DIM, TC, NVP>(p, sc + l, i2h, e);
+            double o[30];
+            double bad = 0.0;
+            const int rc = smooth_flux<VISC, NAX>(e, kp.gas, o, bad);
+            if (rc) {
+                report_error(kp, err_key(kp.stage, 1, cglob_row + i, p, 0, rc), bad);
+#pragma unroll
+                for (int m = 0; m < 30; ++m) o[m] = 0.0;
+            }
+#pragma unroll
+            for (int m = 0; m < 10 * NAX; ++m) vf[(p * 30 + m) * TC + l] = o[m];
         }
+        if (kp.report) return;
+        cp_async_wait<1>();  // this tile's face fluxes
+        __syncthreads();
+
+        // ---- phase C: gather + projection + inverse mass (+ stage-2 combine)
+        constexpr int FT0 = MODE == MODE_STAGE2 ? 1 : 0;
+        constexpr int NITEMS = TC * 5 * (2 - FT0);
+        for (int it = tid; it < NITEMS; it += NT) {
+            const int l = it % TC, vv = it / TC;
+            const int v = vv % 5, ft = FT0 + vv / 5;  // ft: 0 -> F (R), 1 -> Ft (Rt)
+            const int i = i0 + l;
+            if (i >= nx) continue;
+            const double hx = __ldg(kp.dx + i);
+            const double i2h[3] = {__ldg(kp.i2dx + i), i2hy, i2hz};
+            const int row = 5 * ft + v;
+            double R[N];
+#pragma unroll
+            for (int m = 0; m < N; ++m) R[m] = 0.0;
+            // faces (dg.hpp:404-425): + w jac B- F(minus face) - w jac B+ F(plus face),
+            // with the Legendre parity B+(p,n) = (-1)^{n_a} B-(p,n)
+            const double jac[3] = {hy * hz * 0.25, hz * hx * 0.25, hx * hy * 0.25};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int nfp = a == 0 ? CT::NFX : a == 1 ? CT::NFY : CT::NFZ;
+                double acc[N];
+#pragma unroll
+                for (int m = 0; m < N; ++m) acc[m] = 0.0;
+#pragma unroll
+                for (int pf = 0; pf < nfp; ++pf) {
+                    const int r = pf * 10 + row;
+                    double Fm, Fp;
+                    if (a == 0) {
+                        Fm = fx[r * (TC + 1) + l];
+                        Fp = fx[r * (TC + 1) + l + 1];
+                    } else {
+                        const double* fa = a == 1 ? fy : fz;
+                        Fm = fa[r * 2 * TC + l];
+                        Fp = fa[r * 2 * TC + TC + l];
+                    }
+                    const double Dm = Fm - Fp, Sm = Fm + Fp;
+#pragma unroll
+                    for (int m = 0; m < N; ++m) {
+                        const double c = ctab<P, DIM>.fw[a][pf] * ctab<P, DIM>.fB[a][0][pf][m];
+                        const bool odd = ctab<P, DIM>.par[a][m] != 0;
+                        if (c != 0.0) acc[m] += c * (odd ? Sm : Dm);
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < N; ++m) R[m] += jac[a] * acc[m];
+            }
+            // volume (dg.hpp:427-448): + w (h0 h1 h2 / 8) (2/h_a) dB_a F_a
+            const double vol = hx * hy * hz;
+            const double vjac = vol * 0.125;
+#pragma unroll
+            for (int a = 0; a < NAX; ++a) {
+                double acc[N];
+#pragma unroll
+                for (int m = 0; m < N; ++m) acc[m] = 0.0;
+#pragma unroll
+                for (int p = 0; p < NVP; ++p) {
+                    const double F = vf[(p * 30 + a * 10 + row) * TC + l];
+#pragma unroll
+                    for (int m = 0; m < N; ++m) {
+                        const double c = ctab<P, DIM>.vw[p] * ctab<P, DIM>.vdB[p][a][m];
+                        if (c != 0.0) acc[m] += c * F;
+                    }
+                }
+                const double sa = vjac * i2h[a];
+#pragma unroll
+                for (int m = 0; m < N; ++m) R[m] += sa * acc[m];
+            }
+            const long g0 = (long)v * kp.cs + cbase + i;
+            if (MODE == MODE_RESIDUAL) {
+                double* o = ft ? out1 : out0;
+#pragma unroll
+                for (int m = 0; m < N; ++m) o[g0 + (long)(m * 5) * kp.cs] = R[m];
+            } else {
+                // mass_diag (dg.hpp:42-50): 1/M_n = (2nx+1)(2ny+1)(2nz+1)/vol (solver.hpp:49-51)
+                const double ivol = 1.0 / vol;
+                const double c6 = dt * dt / 6.0;
+#pragma unroll
+                for (int m = 0; m < N; ++m) {
+                    const double L = R[m] * (ctab<P, DIM>.massf[m] * ivol);
+                    const long gi = g0 + (long)(m * 5) * kp.cs;
+                    if (MODE == MODE_STAGE1) {
+                        (ft ? out2 : out1)[gi] = L;
+                        lb[(ft * NC + m * 5 + v) * TC + l] = L;
+                    } else {
+                        // q += dt L1 + dt^2/6 (Lt1 + 2 Lt2) (integrator.hpp:72-74)
+                        out0[gi] = __ldg(qn + gi) + (dt * __ldg(L1 + gi) + c6 * (__ldg(Lt1 + gi) + 2.0 * L));
+                    }
+                }
+            }
+        }
+        if (MODE == MODE_STAGE1) {
+            // q* = q + dt/2 L1 + dt^2/8 Lt1 (integrator.hpp:69-70) from shared memory
+            __syncthreads();
+            for (int e = tid; e < NC * TC; e += NT) {
+                const int l = e % TC, comp = e / TC;
+                if (i0 + l >= nx) continue;
+                out0[comp * kp.cs + cbase + i0 + l] =
+                    sc[comp * TC + l] + 0.5 * dt * lb[comp * TC + l] + 0.125 * dt * dt * lb[(NC + comp) * TC + l];
+            }
+        }
+        __syncthreads();  // buffers of this tile are free for the next prefetch
     }
+    cp_async_wait<0>();
 }
 
 }  // namespace hgks_dev

@@ -1,0 +1,113 @@
+"""Summarise gpurun_out/ ncu artefacts into profiles/<tag>_*.{md,json}.
+
+  python tools/profile_summary.py r01
+reads gpurun_out/launches.csv (gpu__time_duration per launch), the
+--set full reports gpurun_out/prof_face.ncu-rep / prof_cell.ncu-rep and
+gpurun_out/bench.json; writes profiles/<tag>_ncu_summary.md,
+profiles/<tag>_launches.csv and profiles/face_kernel_traffic.json (read by
+bench.py for roofline.traffic).
+"""
+import csv
+import json
+import os
+import shutil
+import subprocess
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    return dict(zip(rows[0], rows[2])), dict(zip(rows[0], rows[1]))
+
+
+def num(x):
+    try:
+        return float(str(x).replace(",", ""))
+    except ValueError:
+        return float("nan")
+
+
+def to_bytes(v, unit):
+    f = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+    return num(v) * f
+
+
+def main(tag):
+    os.makedirs(PROF, exist_ok=True)
+    md = [f"# ncu summary {tag}", ""]
+    bench = None
+    if os.path.exists(os.path.join(OUT, "bench.json")):
+        txt = open(os.path.join(OUT, "bench.json")).read().strip().splitlines()
+        bench = json.loads(txt[-1]) if txt else None
+    if bench:
+        md += [f"bench: value {bench['value']:.4g} {bench['unit']}, {bench['ms_per_step']:.2f} ms/step, "
+               f"clocks {bench.get('clocks')}", ""]
+    # launch list (cold-cache, serialised: shares only)
+    lc = os.path.join(OUT, "launches.csv")
+    if os.path.exists(lc):
+        rows = list(csv.reader(open(lc)))
+        hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+        h = rows[hi]
+        ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+        tot, cnt = defaultdict(float), defaultdict(int)
+        for r in rows[hi + 1:]:
+            if len(r) > vi:
+                nm = r[ki].split("(")[0]
+                tot[nm] += num(r[vi])
+                cnt[nm] += 1
+        T = sum(tot.values())
+        md += ["## launch list (ncu gpu__time_duration, `bench.py --steps 2 --warmup 1`)", "",
+               "| kernel | launches | total ms | share |", "|---|---|---|---|"]
+        for k in sorted(tot, key=lambda k: -tot[k]):
+            md.append(f"| `{k}` | {cnt[k]} | {tot[k] / 1e6:.3f} | {100 * tot[k] / T:.1f}% |")
+        md.append("")
+        shutil.copy(lc, os.path.join(PROF, f"{tag}_launches.csv"))
+    traffic = {}
+    for name in ("face", "cell"):
+        rep = os.path.join(OUT, f"prof_{name}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        v, u = raw(rep)
+        rd = to_bytes(v.get("dram__bytes_read.sum"), u.get("dram__bytes_read.sum"))
+        wr = to_bytes(v.get("dram__bytes_write.sum"), u.get("dram__bytes_write.sum"))
+        fp = sum(num(v.get(f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed", 0))
+                 for op in ("dfma", "dmul", "dadd"))
+        dur_ms = num(v.get("gpu__time_duration.sum")) * (1e-3 if u.get("gpu__time_duration.sum") == "usecond" else 1.0)
+        clk = num(v.get("sm__cycles_elapsed.avg.per_second")) * 1e9
+        md += [f"## {name}: `{v.get('Kernel Name', '')[:110]}`", "",
+               f"- duration {dur_ms:.3f} ms, SM clock {clk / 1e9:.3f} GHz, grid {v.get('launch__grid_size')} x "
+               f"{v.get('launch__block_size')}, {v.get('launch__registers_per_thread')} regs/thread",
+               f"- FP64 pipe active {num(v.get('sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active')):.1f}% "
+               f"(fp64 thread-inst/cycle over all SMs {fp:.0f} of {64 * 148})",
+               f"- issue active {num(v.get('smsp__issue_active.avg.pct_of_peak_sustained_active')):.1f}%, warps active "
+               f"{num(v.get('sm__warps_active.avg.pct_of_peak_sustained_active')):.1f}% of 64",
+               f"- DRAM read {rd / 1e6:.1f} MB, write {wr / 1e6:.1f} MB per launch "
+               f"({(rd + wr) / (dur_ms * 1e-3) / 1e9:.0f} GB/s)", ""]
+        st = []
+        for k, x in v.items():
+            if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
+                st.append((num(x), k.replace("smsp__pcsamp_warps_issue_stalled_", "")))
+        tot = sum(a for a, _ in st) or 1.0
+        md.append("- stall samples: " + ", ".join(f"{n} {100 * a / tot:.0f}%" for a, n in sorted(st, reverse=True)[:8]))
+        md.append("")
+        traffic[name] = {"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr, "duration_ms": dur_ms,
+                         "kernel": v.get("Kernel Name", "")}
+    open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
+    if "face" in traffic:
+        t = traffic["face"]
+        json.dump({"tag": tag, "dram_bytes_per_launch": t["dram_bytes_per_launch"], "kernel": t["kernel"],
+                   "note": "one face_kernel launch (one axis); ncu --set full, cold cache"},
+                  open(os.path.join(PROF, "face_kernel_traffic.json"), "w"), indent=1)
+    if bench:
+        json.dump(bench, open(os.path.join(PROF, f"{tag}_bench.json"), "w"), indent=1)
+    print("\n".join(md))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
