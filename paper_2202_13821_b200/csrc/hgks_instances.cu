@@ -21,10 +21,12 @@ struct Launch {
 #if HGKS_FACE_SPLIT
         return FaceSplit<P, DIM, AXIS>::SMEM * (int)sizeof(double);
 #else
-        // staged coefficients of both neighbours + the per-thread flux accumulator
-        return (2 * SH::NC * 32 + 30 * 32 * SH::template nfp<AXIS>()) * (int)sizeof(double);
+        // double-buffered stage of both neighbours' coefficients
+        return 2 * (2 * SH::NC * 32) * (int)sizeof(double);
 #endif
     }
+    // persistent face kernels: resident CTAs on the whole GPU per axis
+    static inline int face_grid[3] = {0, 0, 0};
     static int cell_smem() { return CellTile<P, DIM>::SMEM * (int)sizeof(double); }
     // persistent cell kernel: resident CTAs on the whole GPU (set by configure)
     static inline int cell_grid[3] = {0, 0, 0};
@@ -46,8 +48,16 @@ struct Launch {
         face_kernel_split<P, DIM, VISC, AXIS><<<grid, FS::NT, face_smem<AXIS>(), st>>>(kp, q, f, t[0], t[1], t[2]);
 #else
         constexpr int NFP = SH::template nfp<AXIS>();
-        dim3 grid(report ? 1 : (kp.nx + 31) / 32, report ? 1 : kp.ny, report ? 1 : layers);
-        face_kernel<P, DIM, VISC, AXIS><<<grid, 32 * NFP, face_smem<AXIS>(), st>>>(kp, q, f, t[0], t[1], t[2]);
+        const int ntx = (kp.nx + 31) / 32;
+        const int ntiles = ntx * kp.ny * layers;
+        int first = 0, count = ntiles;
+        int grid = std::min(ntiles, std::max(1, face_grid[AXIS]));
+        if (report) {  // the failing face's tile only
+            first = t[0] + ntx * (t[1] + kp.ny * t[2]);
+            count = 1;
+            grid = 1;
+        }
+        face_kernel<P, DIM, VISC, AXIS><<<grid, 32 * NFP, face_smem<AXIS>(), st>>>(kp, q, f, first, count, 0);
 #endif
     }
     static void face(const KParams& kp, const double* q, double* const f[3], cudaStream_t st,
@@ -110,6 +120,19 @@ struct Launch {
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fns[m], SH::NT_CELL, cell_smem());
             cell_grid[m] = std::max(1, nb) * sms;
         }
+#if !HGKS_FACE_SPLIT
+        const void* ffn[3] = {(const void*)face_kernel<P, DIM, VISC, 0>,
+                              (const void*)face_kernel<P, DIM, VISC, 1>,
+                              (const void*)face_kernel<P, DIM, VISC, 2>};
+        const int fnt[3] = {32 * SH::template nfp<0>(), 32 * SH::template nfp<1>(),
+                            32 * SH::template nfp<2>()};
+        const int fsm[3] = {face_smem<0>(), face_smem<1>(), face_smem<2>()};
+        for (int a = 0; a < 3 && e == cudaSuccess; ++a) {
+            int nb = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ffn[a], fnt[a], fsm[a]);
+            face_grid[a] = std::max(1, nb) * sms;
+        }
+#endif
         return e;
     }
     static KernelSet set() {

@@ -209,116 +209,146 @@ __device__ __forceinline__ void face_pressures_rt(int p, const double* cl, const
     }
 }
 
-// CTA = 32 consecutive faces along x (one lane each) x NFP warps (one face
-// point per warp, so the point index is warp-uniform). The two neighbour
-// cells' coefficients are staged in shared memory SoA [side][comp][lane]
-// with coalesced 256 B row loads.
+// async global->shared copies (cp.async, LDGSTS): the persistent kernels
+// prefetch the next tile while computing the current one
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+                 "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Persistent face kernel. A CTA = NFP warps; each tile is 32 consecutive faces
+// along x (one lane each) at one (j, k), one face point per warp, so the
+// point index is warp-uniform. The two neighbour cells' coefficients of the
+// NEXT tile stream into the other half of a double-buffered shared-memory
+// stage [2][side][comp][32] (cp.async, coalesced 256 B rows) while the
+// current tile's fluxes are computed.
 template <int P, int DIM, bool VISC, int AXIS>
 __global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>(), HGKS_FACE_MINB_P(P))
     face_kernel(KParams kp, const double* __restrict__ q, double* __restrict__ face,
-                int tile_x0, int tile_y0, int tile_z0) {
+                int tile_first, int tile_count, int unused) {
     using SH = Shape<P, DIM>;
     constexpr int NC = SH::NC;
     constexpr int NFP = SH::template nfp<AXIS>();
     constexpr int NT = 32 * NFP;
     constexpr int C1 = (AXIS + 1) % 3, C2 = (AXIS + 2) % 3;
+    constexpr int STG = 2 * NC * 32;  // one stage: [side][comp][32]
     extern __shared__ double smem[];
-    double* sc = smem;  // [2][NC][32]
 
     const int tid = threadIdx.x;
-    const int i0 = (blockIdx.x + tile_x0) * 32;
-    const int j = blockIdx.y + tile_y0;
-    const int k = blockIdx.z + tile_z0;  // local z layer of the plus-side cell
     const int nx = kp.nx, ny = kp.ny;
+    const int ntx = (nx + 31) / 32;
+    const int tile_end = tile_first + tile_count;
+    const int step = kp.report ? tile_count : gridDim.x;
 
-    // stage both neighbours' coefficients: side 0 = minus-side cell, 1 = plus-side
-    for (int e = tid; e < 2 * NC * 32; e += NT) {
-        const int l = e & 31;
-        const int row = e >> 5;
-        const int side = row >= NC;
-        const int comp = row - side * NC;
-        const int i = i0 + l;
-        double v = 0.0;
-        if (i < nx) {
-            int ci = i, cj = j, ck = k;
+    auto prefetch = [&](int t, double* dst) {
+        const int i0 = (t % ntx) * 32, j = (t / ntx) % ny, k = t / (ntx * ny);
+        for (int e = tid; e < STG; e += NT) {
+            const int l = e & 31;
+            const int row = e >> 5;
+            const int side = row >= NC;
+            const int comp = row - side * NC;
+            const int i = i0 + l;
+            const bool ok = i < nx;
+            int ci = ok ? i : 0, cj = j, ck = k;
             if (!side) {
-                if (AXIS == 0) ci = (i == 0 ? nx - 1 : i - 1);
+                if (AXIS == 0) ci = (ci == 0 ? nx - 1 : ci - 1);
                 if (AXIS == 1) cj = (j == 0 ? ny - 1 : j - 1);
                 if (AXIS == 2) ck = k - 1;
             }
-            v = __ldg(q + comp * kp.cs + (long)(ck + 1) * kp.S + (long)cj * nx + ci);
+            cp_async8(dst + e, q + comp * kp.cs + (long)(ck + 1) * kp.S + (long)cj * nx + ci, ok);
         }
-        sc[(side * NC + comp) * 32 + l] = v;
-    }
-    __syncthreads();
+    };
 
     const int lane = tid & 31;
     const int p = tid >> 5;
-    const int i = i0 + lane;
-    if (i >= nx) return;
+    const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
+    if (t0 < tile_end) prefetch(t0, smem);
+    cp_async_commit();
+    int n = 0;
+    for (int t = t0; t < tile_end; t += step, ++n) {
+        double* sc = smem + (n & 1) * STG;
+        if (t + step < tile_end) prefetch(t + step, smem + ((n + 1) & 1) * STG);
+        cp_async_commit();
+        const int i0 = (t % ntx) * 32, j = (t / ntx) % ny, k = t / (ntx * ny);
+        const int i = i0 + lane;
+        cp_async_wait<1>();  // this tile's stage
+        __syncthreads();
+        if (i < nx) {
+            const int im = AXIS == 0 ? (i == 0 ? nx - 1 : i - 1) : i;
+            const int jm = AXIS == 1 ? (j == 0 ? ny - 1 : j - 1) : j;
+            const int km = AXIS == 2 ? k - 1 : k;
+            const double i2hL[3] = {__ldg(kp.i2dx + im), __ldg(kp.i2dy + jm), __ldg(kp.i2dz + km + 1)};
+            const double i2hR[3] = {__ldg(kp.i2dx + i), __ldg(kp.i2dy + j), __ldg(kp.i2dz + k + 1)};
+            const double* cL = sc + lane;
+            const double* cR = sc + NC * 32 + lane;
 
-    const int im = AXIS == 0 ? (i == 0 ? nx - 1 : i - 1) : i;
-    const int jm = AXIS == 1 ? (j == 0 ? ny - 1 : j - 1) : j;
-    const int km = AXIS == 2 ? k - 1 : k;
-    const double i2hL[3] = {__ldg(kp.i2dx + im), __ldg(kp.i2dy + jm), __ldg(kp.i2dz + km + 1)};
-    const double i2hR[3] = {__ldg(kp.i2dx + i), __ldg(kp.i2dy + j), __ldg(kp.i2dz + k + 1)};
-    const double* cL = sc + lane;
-    const double* cR = sc + NC * 32 + lane;
+            // tau = mu / mean trace pressure (dg.hpp:378-383); dt/(2 tau) without a division
+            double tau = 0.0, rh = 0.0;
+            if (VISC) {
+                double pl = 0.0, pr = 0.0;
+                face_pressures_rt<P, DIM, AXIS, NFP>(p, cL, cR, kp.gas, pl, pr);
+                const double ps = pl + pr;
+                tau = kp.two_mu / ps;
+                rh = ps * kp.rh_coef;
+            }
+            const TimeW tw = time_weights_r(tau, kp.inv_dt, rh);
 
-    // tau = mu / mean trace pressure (dg.hpp:378-383); dt/(2 tau) without a division
-    double tau = 0.0, rh = 0.0;
-    if (VISC) {
-        double pl = 0.0, pr = 0.0;
-        face_pressures_rt<P, DIM, AXIS, NFP>(p, cL, cR, kp.gas, pl, pr);
-        const double ps = pl + pr;
-        tau = kp.two_mu / ps;
-        rh = ps * kp.rh_coef;
-    }
-    const TimeW tw = time_weights_r(tau, kp.inv_dt, rh);
-
-    SmemAcc acc{sc + 2 * NC * 32 + tid, NT};  // [30][NT] per-thread accumulator column
-    flux_init(acc);
-    const bool owned = k < kp.nzl;
-    const long f_glob = (long)i + (long)nx * (j + (long)ny * (k + kp.kglob0));
-    const long item = (long)AXIS * kp.ncells_glob + f_glob;
+            FluxAcc acc;
+            flux_init(acc);
+            const bool owned = k < kp.nzl;
+            const long item = (long)AXIS * kp.ncells_glob + (long)i + (long)nx * (j + (long)ny * (k + kp.kglob0));
+            int fail = 0;
 #pragma unroll 1
-    for (int side = 0; side < 2; ++side) {
-        double t[20];
-        face_trace_rt<P, DIM, AXIS, NFP>(p, side, side == 0 ? cL : cR, side == 0 ? i2hL : i2hR, t);
-        double bad = 0.0;
-        const int rc = flux_side<VISC>(t, side, kp.gas, tw, acc, bad);
-        if (rc) {
-            if (owned) report_error(kp, err_key(kp.stage, 0, item, p, side, rc), bad);
-            return;
-        }
-    }
-    double bad = 0.0;
-    const int rc = flux_merge<VISC>(kp.gas, tw, acc, bad);
-    if (rc) {
-        if (owned) report_error(kp, err_key(kp.stage, 0, item, p, 2, rc), bad);
-        return;
-    }
-    if (kp.report) return;
-    // face-local -> global (dg.hpp:336-345)
-    const long fidx = (long)i + (long)nx * (j + (long)ny * k);
-    double* out = face + (long)(p * 10) * kp.fs + fidx;
-    double G[5], Gt[5];
-    G[0] = acc.F(0);
-    G[4] = acc.F(4);
-    G[1 + AXIS] = acc.F(1);
-    G[1 + C1] = acc.F(2);
-    G[1 + C2] = acc.F(3);
-    Gt[0] = acc.Ft(0);
-    Gt[4] = acc.Ft(4);
-    Gt[1 + AXIS] = acc.Ft(1);
-    Gt[1 + C1] = acc.Ft(2);
-    Gt[1 + C2] = acc.Ft(3);
+            for (int side = 0; side < 2 && !fail; ++side) {
+                double tr[20];
+                face_trace_rt<P, DIM, AXIS, NFP>(p, side, side == 0 ? cL : cR, side == 0 ? i2hL : i2hR, tr);
+                double bad = 0.0;
+                const int rc = flux_side<VISC>(tr, side, kp.gas, tw, acc, bad);
+                if (rc) {
+                    if (owned) report_error(kp, err_key(kp.stage, 0, item, p, side, rc), bad);
+                    fail = 1;
+                }
+            }
+            if (!fail) {
+                double bad = 0.0;
+                const int rc = flux_merge<VISC>(kp.gas, tw, acc, bad);
+                if (rc) {
+                    if (owned) report_error(kp, err_key(kp.stage, 0, item, p, 2, rc), bad);
+                    fail = 1;
+                }
+            }
+            if (!fail && !kp.report) {
+                // face-local -> global (dg.hpp:336-345)
+                const long fidx = (long)i + (long)nx * (j + (long)ny * k);
+                double* out = face + (long)(p * 10) * kp.fs + fidx;
+                double G[5], Gt[5];
+                G[0] = acc.F(0);
+                G[4] = acc.F(4);
+                G[1 + AXIS] = acc.F(1);
+                G[1 + C1] = acc.F(2);
+                G[1 + C2] = acc.F(3);
+                Gt[0] = acc.Ft(0);
+                Gt[4] = acc.Ft(4);
+                Gt[1 + AXIS] = acc.Ft(1);
+                Gt[1 + C1] = acc.Ft(2);
+                Gt[1 + C2] = acc.Ft(3);
 #pragma unroll
-    for (int v = 0; v < 5; ++v) {
-        out[v * kp.fs] = G[v];
-        out[(5 + v) * kp.fs] = Gt[v];
+                for (int v = 0; v < 5; ++v) {
+                    out[v * kp.fs] = G[v];
+                    out[(5 + v) * kp.fs] = Gt[v];
+                }
+                if (kp.count_fluxes && owned) atomicAdd(kp.flux_count, 1ull);
+            }
+        }
+        __syncthreads();  // this stage is free for the prefetch two tiles ahead
     }
-    if (kp.count_fluxes && owned) atomicAdd(kp.flux_count, 1ull);
+    cp_async_wait<0>();
 }
 
 // ------------------------------------------------- split-side face kernel
@@ -509,19 +539,6 @@ __device__ __forceinline__ void vol_eval_rt(int p, const double* c, const double
         if (p == PT) vol_eval<P, DIM, PT, TC>(c, i2h, e);
         else vol_eval_rt<P, DIM, TC, NVP, PT + 1>(p, c, i2h, e);
     }
-}
-
-// async global->shared copies (cp.async, LDGSTS): the persistent kernels
-// prefetch the next tile while computing the current one
-__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
-                 "r"(valid ? 8 : 0));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
 // shared-memory plan of one cell-kernel CTA (doubles)
