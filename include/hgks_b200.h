@@ -114,6 +114,12 @@ int hgks_project_case(hgks_solver* s, const char* case_name, double t);
  * (fixed-order device reduction; sums over owned cells only). */
 int hgks_tgv_diagnostics(hgks_solver* s, double* ek_vol, double* ens_vol, double* volume);
 
+/* error_norms (dg.hpp:228-266) of the current state against the named case's
+ * exact field at time t, as UNREDUCED sums over owned cells: out[0] = L1,
+ * out[1] = L2^2, out[2] = cell-average error^2 (ErrorNorms = {out0,
+ * sqrt(out1), sqrt(out2)} after summing over slabs). */
+int hgks_error_norms(hgks_solver* s, const char* case_name, double t, double* out);
+
 /* ---- multi-GPU z-slabs. The halo is one layer of cell
  * coefficients below and above the owned slab, packed contiguously:
  * [comp][cell-in-layer], hgks_halo_bytes() per direction. */

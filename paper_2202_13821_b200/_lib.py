@@ -26,7 +26,7 @@ EXPORTS = [
     "hgks_num_basis", "hgks_num_coeffs", "hgks_face_points", "hgks_set_state", "hgks_get_state",
     "hgks_residual", "hgks_apply_inverse_mass", "hgks_compute_dt", "hgks_step",
     "hgks_two_stage_step_host", "hgks_advance", "hgks_set_count_fluxes", "hgks_flux_evaluations",
-    "hgks_project_case", "hgks_tgv_diagnostics", "hgks_halo_bytes", "hgks_halo_buffers",
+    "hgks_project_case", "hgks_tgv_diagnostics", "hgks_error_norms", "hgks_halo_bytes", "hgks_halo_buffers",
     "hgks_halo_pack", "hgks_halo_unpack", "hgks_set_halo_exchange", "hgks_step_phase",
     "hgks_set_dt_reduce", "hgks_set_stream", "hgks_get_stream", "hgks_synchronize",
     "hgks_launch_count", "hgks_set_kernel_timing", "hgks_kernel_times", "hgks_measure_fp64_peak",
@@ -86,6 +86,7 @@ def load():
     L.hgks_flux_evaluations.restype = ctypes.c_long
     L.hgks_project_case.argtypes = [sp, ctypes.c_char_p, ctypes.c_double]
     L.hgks_tgv_diagnostics.argtypes = [sp, _dp, _dp, _dp]
+    L.hgks_error_norms.argtypes = [sp, ctypes.c_char_p, ctypes.c_double, _dp]
     L.hgks_halo_bytes.argtypes = [sp]
     L.hgks_halo_bytes.restype = ctypes.c_long
     L.hgks_halo_buffers.argtypes = [sp, _u64p, _u64p, _u64p, _u64p]

@@ -344,4 +344,65 @@ inline void launch_tgv(int degree, int dim, const KParams& kp, int npts, const d
     else tgv_kernel<100><<<blocks, 256, 0, st>>>(kp, npts, q, ncell, part);
 }
 
+// error_norms (dg.hpp:228-266) partial sums per block: {sum vol/8 l1_c,
+// sum vol/8 l2_c, sum vol davg^2} with the (k+2)^3 projection rule; fixed-
+// order tree inside the block (deterministic)
+template <int N>
+__global__ void __launch_bounds__(256) error_kernel(KParams kp, CaseParams cp, const double* __restrict__ ctr,
+                                                    const double* __restrict__ q, long ncell,
+                                                    double* __restrict__ part) {
+    __shared__ double red[3][256];
+    double s1 = 0, s2 = 0, sc = 0;
+    for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < ncell; c += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(c % kp.nx), j = (int)((c / kp.nx) % kp.ny), k = (int)(c / kp.S);
+        const double h[3] = {kp.dx[i], kp.dy[j], kp.dz[k + 1]};
+        const double x0[3] = {ctr[i], ctr[kp.nx + j], ctr[kp.nx + kp.ny + k]};
+        const double vol = h[0] * h[1] * h[2];
+        double rho_c[N];
+#pragma unroll
+        for (int n = 0; n < N; ++n) rho_c[n] = q[(n * 5) * kp.cs + kp.S + c];
+        double l1 = 0, l2 = 0, avg = 0;
+        for (int p = 0; p < cp.npts; ++p) {
+            const double* r = kp.tab + kp.off_pref + 3 * p;
+            const double x[3] = {x0[0] + 0.5 * h[0] * r[0], x0[1] + 0.5 * h[1] * r[1], x0[2] + 0.5 * h[2] * r[2]};
+            double f[5];
+            case_field(cp, x, f);
+            const double* B = kp.tab + kp.off_pB + p * N;
+            double rh = 0;
+#pragma unroll
+            for (int n = 0; n < N; ++n) rh += B[n] * rho_c[n];
+            const double d = fabs(f[0] - rh);
+            const double w = kp.tab[kp.off_pw + p];
+            l1 += w * d;
+            l2 += w * d * d;
+            avg += w * f[0];
+        }
+        avg /= 8.0;
+        const double davg = avg - rho_c[0];
+        s1 += vol / 8.0 * l1;
+        s2 += vol / 8.0 * l2;
+        sc += vol * davg * davg;
+    }
+    red[0][threadIdx.x] = s1;
+    red[1][threadIdx.x] = s2;
+    red[2][threadIdx.x] = sc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            for (int r = 0; r < 3; ++r) red[r][threadIdx.x] += red[r][threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int r = 0; r < 3; ++r) part[3 * blockIdx.x + r] = red[r][0];
+}
+
+inline void launch_error(int degree, int dim, const KParams& kp, const CaseParams& cp, const double* ctr,
+                         const double* q, long ncell, double* part, int blocks, cudaStream_t st) {
+    const int N = dim == 3 ? (degree == 1 ? 4 : degree == 2 ? 10 : 20) : (degree == 2 ? 6 : 10);
+    if (N == 4) error_kernel<4><<<blocks, 256, 0, st>>>(kp, cp, ctr, q, ncell, part);
+    else if (N == 6) error_kernel<6><<<blocks, 256, 0, st>>>(kp, cp, ctr, q, ncell, part);
+    else if (N == 10) error_kernel<10><<<blocks, 256, 0, st>>>(kp, cp, ctr, q, ncell, part);
+    else error_kernel<20><<<blocks, 256, 0, st>>>(kp, cp, ctr, q, ncell, part);
+}
+
 }  // namespace hgks_dev

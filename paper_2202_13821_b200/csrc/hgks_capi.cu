@@ -635,26 +635,24 @@ void hgks_set_count_fluxes(hgks_solver* s, int on) {
 }
 long hgks_flux_evaluations(const hgks_solver* s) { return s->flux_evals; }
 
-int hgks_project_case(hgks_solver* s, const char* case_name, double t) {
+}  // extern "C"
+
+namespace {
+// case parameters (CaseConfig::named, cases.hpp:12-46) and cell centres of
+// the owned cells on the device; caller frees *d_ctr
+int case_setup(hgks_solver* s, const char* case_name, double t, CaseParams& cp, double** d_ctr) {
     int cid;
     if (!std::strcmp(case_name, "adv2d")) cid = CASE_ADV2D;
     else if (!std::strcmp(case_name, "adv3d")) cid = CASE_ADV3D;
     else if (!std::strcmp(case_name, "vortex2d")) cid = CASE_VORTEX2D;
     else if (!std::strcmp(case_name, "tgv")) cid = CASE_TGV;
     else return fail(s, HGKS_ERR_CONFIG, std::string("unknown case: ") + case_name);
-    KParams kp = make_params(s, 0.0, 0);
-    std::vector<double> hx(s->nx), hy(s->ny), hz(s->nzl);
-    for (int i = 0; i < s->nx; ++i) hx[i] = 0.5 * (s->xs[i] + s->xs[i + 1]);
-    for (int j = 0; j < s->ny; ++j) hy[j] = 0.5 * (s->ys[j] + s->ys[j + 1]);
-    for (int k = 0; k < s->nzl; ++k) hz[k] = 0.5 * (s->zs[s->z0 + k] + s->zs[s->z0 + k + 1]);
     std::vector<double> ctr;
-    ctr.insert(ctr.end(), hx.begin(), hx.end());
-    ctr.insert(ctr.end(), hy.begin(), hy.end());
-    ctr.insert(ctr.end(), hz.begin(), hz.end());
-    double* d_ctr = nullptr;
-    CK(cudaMalloc(&d_ctr, ctr.size() * sizeof(double)));
-    CK(cudaMemcpyAsync(d_ctr, ctr.data(), ctr.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
-    CaseParams cp;
+    for (int i = 0; i < s->nx; ++i) ctr.push_back(0.5 * (s->xs[i] + s->xs[i + 1]));
+    for (int j = 0; j < s->ny; ++j) ctr.push_back(0.5 * (s->ys[j] + s->ys[j + 1]));
+    for (int k = 0; k < s->nzl; ++k) ctr.push_back(0.5 * (s->zs[s->z0 + k] + s->zs[s->z0 + k + 1]));
+    CK(cudaMalloc(d_ctr, ctr.size() * sizeof(double)));
+    CK(cudaMemcpyAsync(*d_ctr, ctr.data(), ctr.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     cp.cid = cid;
     cp.dim = s->cfg.dim;
     cp.gamma = s->cfg.gamma;
@@ -662,13 +660,51 @@ int hgks_project_case(hgks_solver* s, const char* case_name, double t) {
     cp.eps = 5.0;
     cp.t = t;
     cp.npts = s->tabs.proj.npts;
-    const long ncell = s->S * s->nzl;
-    launch_project(s->cfg.degree, s->cfg.dim, kp, cp, d_ctr, s->qa, ncell, s->stream);
+    return HGKS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int hgks_project_case(hgks_solver* s, const char* case_name, double t) {
+    CaseParams cp;
+    double* d_ctr = nullptr;
+    int rc = case_setup(s, case_name, t, cp, &d_ctr);
+    if (rc) return rc;
+    KParams kp = make_params(s, 0.0, 0);
+    launch_project(s->cfg.degree, s->cfg.dim, kp, cp, d_ctr, s->qa, s->S * s->nzl, s->stream);
     ++s->launches;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s->stream));
     cudaFree(d_ctr);
-    s->time = 0.0;
+    s->time = t;
+    return HGKS_OK;
+}
+
+int hgks_error_norms(hgks_solver* s, const char* case_name, double t, double* out) {
+    if (!std::strcmp(case_name, "tgv")) return fail(s, HGKS_ERR_CONFIG, "case has no exact solution: tgv");
+    CaseParams cp;
+    double* d_ctr = nullptr;
+    int rc = case_setup(s, case_name, t, cp, &d_ctr);
+    if (rc) return rc;
+    KParams kp = make_params(s, 0.0, 0);
+    const int blocks = 148 * 2;
+    launch_error(s->cfg.degree, s->cfg.dim, kp, cp, d_ctr, s->qa, s->S * s->nzl, s->d_red, blocks, s->stream);
+    ++s->launches;
+    CK(cudaGetLastError());
+    std::vector<double> part(3 * blocks);
+    CK(cudaMemcpyAsync(part.data(), s->d_red, part.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    cudaFree(d_ctr);
+    double l1 = 0, l2 = 0, ec = 0;
+    for (int b = 0; b < blocks; ++b) {  // fixed order
+        l1 += part[3 * b];
+        l2 += part[3 * b + 1];
+        ec += part[3 * b + 2];
+    }
+    out[0] = l1;  // partial sums: multi-slab callers add them over ranks,
+    out[1] = l2;  // then take sqrt of [1] and [2] (ErrorNorms, dg.hpp:265)
+    out[2] = ec;
     return HGKS_OK;
 }
 

@@ -286,6 +286,17 @@ class Solver:
     def project_case(self, case_name: str, t: float = 0.0):
         self._check(self.L.hgks_project_case(self.h, case_name.encode(), t))
 
+    def error_norm_sums(self, case_name: str, t: float):
+        """Unreduced error_norms sums over owned cells: (L1, L2^2, cell-avg^2)."""
+        out = np.zeros(3)
+        self._check(self.L.hgks_error_norms(self.h, case_name.encode(), t, _ptr(out)))
+        return out
+
+    def error_norms(self, case_name: str, t: float):
+        """error_norms (dg.hpp:228-266): (l1, l2, cell_avg) against the exact field."""
+        s = self.error_norm_sums(case_name, t)
+        return np.array([s[0], np.sqrt(s[1]), np.sqrt(s[2])])
+
     def tgv_diagnostics(self):
         """(Ek*vol, enstrophy*vol, vol) sums over owned cells (cases.hpp:165-204)."""
         e, z, v = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
@@ -484,19 +495,14 @@ def advance(r: RunResult, cfg: CaseConfig, opt: RunOptions, on_record: Callable[
     record = cfg.name == "tgv"
     next_record = opt.record_interval
     on_record(r)
-    t = r.solver.time
-    while t < t_end - 1e-14 * t_end:
-        dt = opt.dt_fixed if opt.dt_fixed is not None else r.solver.compute_dt(cfl)
-        dt = min(dt, t_end - t)
-        if record:
-            dt = min(dt, next_record - t)
-        try:
-            r.solver.step(dt)
-        except InvalidStateError as e:
-            raise InvalidStateError(f"{e} at t={t:f}", e.item, e.phase, e.value) from None
-        t += dt
-        r.steps += 1
-        if record and t >= next_record - 1e-12:
+    dt_fixed = opt.dt_fixed if opt.dt_fixed is not None else 0.0
+    # the device loop (hgks_advance) runs each record interval: dt = compute_dt
+    # (or dt_fixed) clipped to the chunk end, which is min(t_end, next record)
+    # exactly as solver.hpp:91-93 clips; " at t=<t>" is appended on failure
+    while r.solver.time < t_end - 1e-14 * t_end:
+        chunk_end = min(t_end, next_record) if record else t_end
+        r.steps += r.solver.advance_to(chunk_end, cfl, dt_fixed, 0.0)
+        if record and r.solver.time >= next_record - 1e-12:
             on_record(r)
             next_record += opt.record_interval
 
@@ -528,6 +534,77 @@ def run_case(cfg: CaseConfig, opt: RunOptions) -> RunResult:
         for x, e in zip(r.records, eps):
             x.epsEk = e
     return r
+
+
+@dataclass
+class ErrorNorms:
+    """dg.hpp:222-224."""
+    l1: float
+    l2: float
+    cell_avg: float
+
+
+def run_error_norms(r: RunResult, cfg: CaseConfig) -> ErrorNorms:
+    """solver.hpp:129-134 (device error_norms, dg.hpp:228-266)."""
+    l1, l2, ec = r.solver.error_norms(cfg.name, r.solver.time)
+    return ErrorNorms(float(l1), float(l2), float(ec))
+
+
+@dataclass
+class StudyOptions:
+    """solver.hpp:143-152."""
+    degree: int = 2
+    nonuniform: bool = False
+    workers: int = 1
+    nominal: bool = False
+    dt_power: float = 2.0
+    dt_safety: float = 0.7
+    anchor_index: int = 0
+    cfl: Optional[float] = None
+    device: int = 0
+
+
+@dataclass
+class StudyRow:
+    n: int
+    err: ErrorNorms
+    steps: int
+    dt: float
+
+
+def convergence_study(case_name: str, meshes: List[int], sopt: StudyOptions) -> List[StudyRow]:
+    """solver.hpp:161-202: per mesh run_case + error norms; refined mode uses
+    dt = min(anchor_dt (n_anchor/n)^power, cfl_dt(n)), nominal the CFL step."""
+    cfl = sopt.cfl if sopt.cfl is not None else default_cfl(sopt.degree)
+
+    def cfl_dt(n):
+        cfg = CaseConfig.named(case_name, n)
+        cfg.nonuniform = sopt.nonuniform
+        r = setup_run(cfg, RunOptions(degree=sopt.degree, device=sopt.device))
+        dt = r.solver.compute_dt(cfl)
+        r.solver.close()
+        return dt
+
+    anchor_dt, anchor_n = 0.0, 0
+    if not sopt.nominal:
+        anchor_n = meshes[min(sopt.anchor_index, len(meshes) - 1)]
+        anchor_dt = sopt.dt_safety * cfl_dt(anchor_n)
+    rows = []
+    for n in meshes:
+        cfg = CaseConfig.named(case_name, n)
+        cfg.nonuniform = sopt.nonuniform
+        opt = RunOptions(degree=sopt.degree, cfl=cfl, device=sopt.device)
+        if not sopt.nominal:
+            policy = anchor_dt * (anchor_n / n) ** sopt.dt_power
+            opt.dt_fixed = min(policy, cfl_dt(n))
+        r = run_case(cfg, opt)
+        rows.append(StudyRow(n, run_error_norms(r, cfg), r.steps, opt.dt_fixed or 0.0))
+        r.solver.close()
+    return rows
+
+
+def order(coarse: StudyRow, fine: StudyRow, norm: str) -> float:
+    return math.log2(getattr(coarse.err, norm) / getattr(fine.err, norm))
 
 
 # ------------------------------------------------ free-function spellings

@@ -1,0 +1,119 @@
+"""The reference's acceptance criteria (proj/tests/acceptance.cpp:83-252),
+replayed on the B200 path: the paper's published convergence tables
+ and the Taylor-Green analytics. These runs take hours on
+the CPU reference; they take seconds here. Tolerances are the reference's.
+"""
+import math
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def study(P, case, meshes, **kw):
+    return P.solver.convergence_study(case, meshes, P.solver.StudyOptions(**kw))
+
+
+def test_criterion1_adv2d_p2_paper_table(hgks):
+    """acceptance.cpp:83-98: adv2d P2, dt ~ h^2 (safety 0.7): eL1 within 30% of
+    the paper and orders within 0.2."""
+    P = hgks
+    rows = study(P, "adv2d", [8, 16, 32, 64], degree=2, dt_power=2.0, dt_safety=0.7)
+    paper_l1 = [1.2632e-2, 1.2982e-3, 1.5215e-4, 1.8633e-5]
+    paper_o = [3.28, 3.09, 3.03]
+    for r, pl in zip(rows, paper_l1):
+        assert 0.7 < r.err.l1 / pl < 1.3, (r.n, r.err.l1, pl)
+    for i in range(3):
+        o = P.solver.order(rows[i], rows[i + 1], "l1")
+        assert abs(o - paper_o[i]) <= 0.2, (i, o)
+    # criterion 3 (acceptance.cpp:139-147): cell-average super-convergence
+    for i in range(3):
+        assert P.solver.order(rows[i], rows[i + 1], "cell_avg") >= 3.9
+
+
+@pytest.mark.parametrize("degree,nonuniform,l1_16,l1_32,l2_16,l2_32", [
+    (2, False, 2.9226e-3, 2.9518e-4, 1.1441e-3, 1.1712e-4),
+    (2, True, 3.1274e-3, 3.1367e-4, 1.2335e-3, 1.2516e-4),
+    (3, False, 9.0567e-5, 5.6787e-6, 5.3092e-5, 3.3471e-6),
+    (3, True, 1.0973e-4, 6.7226e-6, 5.4167e-5, 3.3516e-6),
+])
+def test_criterion4_adv3d_paper_table(hgks, degree, nonuniform, l1_16, l1_32, l2_16, l2_32):
+    """acceptance.cpp:149-182 (BASELINE config C2): 3-D advection, nominal CFL
+    steps on 8/16/32^3; L1/L2 orders k+1 +- 0.3 (the paper's orders).
+
+    Magnitudes are pinned to the REFERENCE's own study outputs
+    (tests/golden/acceptance_ref.json, make_acceptance_golden.py) at 1e-6:
+    the reference itself lands outside acceptance.cpp's 30% band around the
+    paper's table for P2 uniform 16^3 (L1 3.896e-3 vs 2.9226e-3, ratio 1.333),
+    so the paper ratio is reported, not asserted."""
+    import json
+    import os
+    P = hgks
+    rows = study(P, "adv3d", [8, 16, 32], degree=degree, nominal=True, nonuniform=nonuniform)
+    target = degree + 1.0
+    o1 = P.solver.order(rows[1], rows[2], "l1")
+    o2 = P.solver.order(rows[1], rows[2], "l2")
+    print(f"P{degree} nonuniform={nonuniform}: orders L1 {o1:.3f} L2 {o2:.3f}; paper ratios "
+          f"{rows[1].err.l1 / l1_16:.3f} {rows[2].err.l1 / l1_32:.3f} {rows[1].err.l2 / l2_16:.3f} "
+          f"{rows[2].err.l2 / l2_32:.3f}")
+    assert abs(o1 - target) <= 0.3
+    assert abs(o2 - target) <= 0.3
+    gold = os.path.join(os.path.dirname(__file__), "golden", "acceptance_ref.json")
+    key = f"adv3d_p{degree}_{'nonuniform' if nonuniform else 'uniform'}"
+    ref = json.load(open(gold)).get(key, []) if os.path.exists(gold) else []
+    assert ref, f"no reference golden rows for {key}"
+    for g in ref:
+        mine = next(r for r in rows if r.n == g["n"])
+        assert mine.steps == g["steps"]
+        for norm in ("l1", "l2", "cell_avg"):
+            assert abs(getattr(mine.err, norm) - g[norm]) <= 1e-6 * g[norm], (g["n"], norm)
+
+
+def test_criterion5_vortex_p2_orders(hgks):
+    """acceptance.cpp:184-195: isotropic vortex P2, nominal steps, 20..160^2."""
+    P = hgks
+    rows = study(P, "vortex2d", [20, 40, 80, 160], degree=2, nominal=True)
+    paper = [2.94, 2.82, 2.95]
+    for i in range(3):
+        o = P.solver.order(rows[i], rows[i + 1], "l1")
+        assert abs(o - paper[i]) <= 0.3, (i, o)
+
+
+def test_criterion6_tgv32_analytics(hgks):
+    """acceptance.cpp:206-252: TGV P2 32^3 to t = 10, records every 0.05:
+    Ek(0) = 0.125, epsZeta(0) = 4.6875e-4 (2%), Ek monotone, and the
+    integrated central-difference dissipation matches the Ek drop to 1%."""
+    P = hgks
+    cfg = P.CaseConfig.named("tgv", 32)
+    r = P.run_case(cfg, P.RunOptions(degree=2, record_interval=0.05))
+    recs = r.records
+    assert len(recs) == 201
+    assert abs(recs[0].Ek - 0.125) <= 1e-6
+    assert abs(recs[0].epsZeta - 4.6875e-4) <= 0.02 * 4.6875e-4
+    assert all(b.Ek <= a.Ek + 1e-12 for a, b in zip(recs, recs[1:]))
+    integral = sum(0.5 * (b.epsEk + a.epsEk) * (b.t - a.t) for a, b in zip(recs, recs[1:]))
+    drop = recs[0].Ek - recs[-1].Ek
+    assert abs(integral - drop) <= 0.01 * drop
+    assert abs(recs[-1].t - 10.0) <= 1e-9
+    # the physics: the dissipation peak of the Re=1600 TGV sits near t ~ 8-9
+    peak = max(recs, key=lambda x: x.epsEk)
+    assert 6.0 < peak.t < 10.0 and math.isfinite(peak.epsEk)
+
+
+def test_error_norms_match_oracle(hgks, oracle_mod):
+    """device error_norms (dg.hpp:228-266) vs the oracle after a few steps."""
+    P, O = hgks, oracle_mod
+    for case, n, deg in [("adv3d", 6, 2), ("vortex2d", 8, 3)]:
+        cfg = P.CaseConfig.named(case, n)
+        r = P.setup_run(cfg, P.RunOptions(degree=deg))
+        o = O.Oracle(case, n, deg)
+        r.solver.set_state(o.state.copy(), 0.0)
+        for _ in range(3):
+            dt = o.compute_dt(0.15 if deg == 2 else 0.09)
+            o.step(dt)
+            r.solver.step(dt)
+        t = r.solver.time
+        a = r.solver.error_norms(case, t)
+        b = o.error_norms(t)
+        for x, y in zip(a, b):
+            assert abs(x - y) <= 1e-9 * abs(y)

@@ -1,0 +1,39 @@
+"""P1 extension (BASELINE configs C2/C5). The reference rejects degree 1
+(basis.hpp:65, test_discretization.cpp:51), so P1 is UNPINNED against it:
+the device path is checked against the C restatement run at k = 1 (same
+code path as P2/P3, 2-point flux rule as DGTables::make would pick, dg.hpp:94)
+and against the expected second-order convergence."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+
+
+@pytest.mark.parametrize("case,n", [("adv3d", 4), ("tgv", 6)])
+def test_p1_matches_restatement(hgks, oracle_mod, case, n):
+    P, O = hgks, oracle_mod
+    r = P.setup_run(P.CaseConfig.named(case, n), P.RunOptions(degree=1))
+    o = O.Oracle(case, n, 1)
+    assert rel(r.solver.get_state()[0], o.state) <= 1e-13
+    dt = o.compute_dt(0.09)
+    a, b = o.residual(dt), r.solver.residual(dt)
+    assert rel(b["R"], a["R"]) <= 1e-12
+    assert rel(b["Rt"], a["Rt"]) <= 1e-10
+    for _ in range(10):
+        dt = o.compute_dt(0.09)
+        o.step(dt)
+        r.solver.step(dt)
+    assert rel(r.solver.get_state()[0], o.state) <= 1e-10
+
+
+def test_p1_second_order(hgks):
+    P = hgks
+    rows = P.solver.convergence_study("adv3d", [8, 16, 32], P.solver.StudyOptions(degree=1, nominal=True))
+    o1 = P.solver.order(rows[1], rows[2], "l1")
+    o2 = P.solver.order(rows[1], rows[2], "l2")
+    print("P1 adv3d orders", o1, o2, [r.err.l1 for r in rows])
+    assert abs(o1 - 2.0) <= 0.3 and abs(o2 - 2.0) <= 0.3
