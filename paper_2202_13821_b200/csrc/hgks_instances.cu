@@ -18,12 +18,8 @@ struct Launch {
     using SH = Shape<P, DIM>;
     template <int AXIS = 2>
     static int face_smem() {
-#if HGKS_FACE_SPLIT
-        return FaceSplit<P, DIM, AXIS>::SMEM * (int)sizeof(double);
-#else
         // double-buffered stage of both neighbours' coefficients
         return 2 * (2 * SH::NC * 32) * (int)sizeof(double);
-#endif
     }
     // persistent face kernels: resident CTAs on the whole GPU per axis
     static inline int face_grid[3] = {0, 0, 0};
@@ -41,12 +37,6 @@ struct Launch {
             t[1] = tile[1];
             t[2] = tile[2];
         }
-#if HGKS_FACE_SPLIT
-        using FS = FaceSplit<P, DIM, AXIS>;
-        dim3 grid(report ? FS::NGRP : ((kp.nx + 31) / 32) * FS::NGRP, report ? 1 : kp.ny,
-                  report ? 1 : layers);
-        face_kernel_split<P, DIM, VISC, AXIS><<<grid, FS::NT, face_smem<AXIS>(), st>>>(kp, q, f, t[0], t[1], t[2]);
-#else
         constexpr int NFP = SH::template nfp<AXIS>();
         const int ntx = (kp.nx + 31) / 32;
         const int ntiles = ntx * kp.ny * layers;
@@ -58,7 +48,6 @@ struct Launch {
             grid = 1;
         }
         face_kernel<P, DIM, VISC, AXIS><<<grid, 32 * NFP, face_smem<AXIS>(), st>>>(kp, q, f, first, count, 0);
-#endif
     }
     static void face(const KParams& kp, const double* q, double* const f[3], cudaStream_t st,
                      int report, const int* tile) {
@@ -96,15 +85,9 @@ struct Launch {
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         };
-#if HGKS_FACE_SPLIT
-        set((const void*)face_kernel_split<P, DIM, VISC, 0>, face_smem<0>());
-        set((const void*)face_kernel_split<P, DIM, VISC, 1>, face_smem<1>());
-        set((const void*)face_kernel_split<P, DIM, VISC, 2>, face_smem<2>());
-#else
         set((const void*)face_kernel<P, DIM, VISC, 0>, face_smem<0>());
         set((const void*)face_kernel<P, DIM, VISC, 1>, face_smem<1>());
         set((const void*)face_kernel<P, DIM, VISC, 2>, face_smem<2>());
-#endif
         set((const void*)cell_kernel<P, DIM, VISC, MODE_RESIDUAL>, cell_smem());
         set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE1>, cell_smem());
         set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE2>, cell_smem());
@@ -120,7 +103,6 @@ struct Launch {
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fns[m], SH::NT_CELL, cell_smem());
             cell_grid[m] = std::max(1, nb) * sms;
         }
-#if !HGKS_FACE_SPLIT
         const void* ffn[3] = {(const void*)face_kernel<P, DIM, VISC, 0>,
                               (const void*)face_kernel<P, DIM, VISC, 1>,
                               (const void*)face_kernel<P, DIM, VISC, 2>};
@@ -132,7 +114,6 @@ struct Launch {
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ffn[a], fnt[a], fsm[a]);
             face_grid[a] = std::max(1, nb) * sms;
         }
-#endif
         return e;
     }
     static KernelSet set() {

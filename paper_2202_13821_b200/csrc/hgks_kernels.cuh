@@ -22,13 +22,6 @@
 #ifndef HGKS_FACE_MINB
 #define HGKS_FACE_MINB 3
 #endif
-// 1: two threads per face point (face_kernel_split); 0: one (face_kernel).
-// Measured on B200 (TGV P2 128^3): the single-thread kernel at 3 CTAs/SM is
-// faster (16.5 vs 19.5 ms per step for the face passes); the split variant
-// is kept as a build option for the record.
-#ifndef HGKS_FACE_SPLIT
-#define HGKS_FACE_SPLIT 0
-#endif
 // P3 face CTAs have 9 warps: one CTA per SM keeps them spill-free
 #define HGKS_FACE_MINB_P(P) ((P) == 3 ? 1 : HGKS_FACE_MINB)
 // cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
@@ -164,28 +157,6 @@ __device__ __forceinline__ void face_trace(const double* __restrict__ c, const d
     }
 }
 
-// value-only traces of both sides at PT -> pressures (for tau, dg.hpp:378-383)
-template <int P, int DIM, int AXIS, int PT>
-__device__ __forceinline__ void face_pressures(const double* __restrict__ cl,
-                                               const double* __restrict__ cr, const GasC& g,
-                                               double& pl, double& pr) {
-    using SH = Shape<P, DIM>;
-    constexpr int N = SH::N, NQ = SH::NQ;
-    double ql[5] = {0, 0, 0, 0, 0}, qr[5] = {0, 0, 0, 0, 0};
-#pragma unroll
-    for (int n = 0; n < N; ++n) {
-        const double bl = ctab<P, DIM>.fB[AXIS][1][PT][n];
-        const double br = ctab<P, DIM>.fB[AXIS][0][PT][n];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-            ql[v] += bl * cl[(n * 5 + v) * 32];
-            qr[v] += br * cr[(n * 5 + v) * 32];
-        }
-    }
-    pl = pressure_q(ql, g);
-    pr = pressure_q(qr, g);
-}
-
 // runtime point index -> compile-time instantiation (warp-uniform branch)
 template <int P, int DIM, int AXIS, int NFP, int PT = 0>
 __device__ __forceinline__ void face_trace_rt(int p, int side, const double* c, const double* i2h,
@@ -197,15 +168,6 @@ __device__ __forceinline__ void face_trace_rt(int p, int side, const double* c, 
         } else {
             face_trace_rt<P, DIM, AXIS, NFP, PT + 1>(p, side, c, i2h, t);
         }
-    }
-}
-
-template <int P, int DIM, int AXIS, int NFP, int PT = 0>
-__device__ __forceinline__ void face_pressures_rt(int p, const double* cl, const double* cr,
-                                                  const GasC& g, double& pl, double& pr) {
-    if constexpr (PT < NFP) {
-        if (p == PT) face_pressures<P, DIM, AXIS, PT>(cl, cr, g, pl, pr);
-        else face_pressures_rt<P, DIM, AXIS, NFP, PT + 1>(p, cl, cr, g, pl, pr);
     }
 }
 
@@ -288,36 +250,31 @@ __global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>(), HGKS
             const double* cL = sc + lane;
             const double* cR = sc + NC * 32 + lane;
 
-            // tau = mu / mean trace pressure (dg.hpp:378-383); dt/(2 tau) without a division
-            double tau = 0.0, rh = 0.0;
-            if (VISC) {
-                double pl = 0.0, pr = 0.0;
-                face_pressures_rt<P, DIM, AXIS, NFP>(p, cL, cR, kp.gas, pl, pr);
-                const double ps = pl + pr;
-                tau = kp.two_mu / ps;
-                rh = ps * kp.rh_coef;
-            }
-            const TimeW tw = time_weights_r(tau, kp.inv_dt, rh);
-
             FluxAcc acc;
             flux_init(acc);
             const bool owned = k < kp.nzl;
             const long item = (long)AXIS * kp.ncells_glob + (long)i + (long)nx * (j + (long)ny * (k + kp.kglob0));
             int fail = 0;
+            double psum = 0.0;  // p_l + p_r of the traces
 #pragma unroll 1
             for (int side = 0; side < 2 && !fail; ++side) {
                 double tr[20];
                 face_trace_rt<P, DIM, AXIS, NFP>(p, side, side == 0 ? cL : cR, side == 0 ? i2hL : i2hR, tr);
-                double bad = 0.0;
-                const int rc = flux_side<VISC>(tr, side, kp.gas, tw, acc, bad);
+                double bad = 0.0, ps = 0.0;
+                const int rc = flux_side<VISC>(tr, side, kp.gas, acc, ps, bad);
+                psum += ps;
                 if (rc) {
                     if (owned) report_error(kp, err_key(kp.stage, 0, item, p, side, rc), bad);
                     fail = 1;
                 }
             }
+            double F[5], Ft[5];
             if (!fail) {
+                // tau = mu / mean trace pressure (dg.hpp:378-383); dt/(2 tau) without a division
+                const double tau = VISC ? kp.two_mu / psum : 0.0;
+                const TimeW tw = time_weights_r(tau, kp.inv_dt, VISC ? psum * kp.rh_coef : 0.0);
                 double bad = 0.0;
-                const int rc = flux_merge<VISC>(kp.gas, tw, acc, bad);
+                const int rc = flux_merge<VISC>(kp.gas, tw, acc, F, Ft, bad);
                 if (rc) {
                     if (owned) report_error(kp, err_key(kp.stage, 0, item, p, 2, rc), bad);
                     fail = 1;
@@ -328,16 +285,16 @@ __global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>(), HGKS
                 const long fidx = (long)i + (long)nx * (j + (long)ny * k);
                 double* out = face + (long)(p * 10) * kp.fs + fidx;
                 double G[5], Gt[5];
-                G[0] = acc.F(0);
-                G[4] = acc.F(4);
-                G[1 + AXIS] = acc.F(1);
-                G[1 + C1] = acc.F(2);
-                G[1 + C2] = acc.F(3);
-                Gt[0] = acc.Ft(0);
-                Gt[4] = acc.Ft(4);
-                Gt[1 + AXIS] = acc.Ft(1);
-                Gt[1 + C1] = acc.Ft(2);
-                Gt[1 + C2] = acc.Ft(3);
+                G[0] = F[0];
+                G[4] = F[4];
+                G[1 + AXIS] = F[1];
+                G[1 + C1] = F[2];
+                G[1 + C2] = F[3];
+                Gt[0] = Ft[0];
+                Gt[4] = Ft[4];
+                Gt[1 + AXIS] = Ft[1];
+                Gt[1 + C1] = Ft[2];
+                Gt[1 + C2] = Ft[3];
 #pragma unroll
                 for (int v = 0; v < 5; ++v) {
                     out[v * kp.fs] = G[v];
@@ -349,154 +306,6 @@ __global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>(), HGKS
         __syncthreads();  // this stage is free for the prefetch two tiles ahead
     }
     cp_async_wait<0>();
-}
-
-// ------------------------------------------------- split-side face kernel
-// Each face point is computed by TWO threads: warp w of the CTA handles side
-// w / PG (0 = left, 1 = right) of point grp*PG + w % PG for 32 consecutive
-// faces. The side passes run in parallel (half the live state per thread,
-// twice the threads per point); their 30-double contributions meet in
-// shared memory, both threads build the merged state, and the merge work
-// is split (part A: g0 + Abar terms, part B: abar term). Results are summed
-// in a fixed order, so they are deterministic.
-template <int P, int DIM, int AXIS>
-struct FaceSplit {
-    static constexpr int NFP = Shape<P, DIM>::template nfp<AXIS>();
-    static constexpr int PG = (NFP % 3 == 0) ? 3 : 2;  // points per CTA
-    static constexpr int NGRP = NFP / PG;              // CTAs per 32-face tile
-    static constexpr int NT = 64 * PG;
-    static constexpr int NC = Shape<P, DIM>::NC;
-    // doubles: staging [2][NC][32] aliased after the traces by
-    // xs [2][30][PG][32] + ys [2][10][PG][32]; ps [2][PG][32] separate
-    static constexpr int STAGE = 2 * NC * 32;
-    static constexpr int XY = (2 * 30 + 2 * 10) * PG * 32;
-    static constexpr int SMEM = (STAGE > XY ? STAGE : XY) + 2 * PG * 32;
-};
-
-template <int P, int DIM, bool VISC, int AXIS>
-__global__ void __launch_bounds__(FaceSplit<P, DIM, AXIS>::NT, HGKS_FACE_MINB_P(P))
-    face_kernel_split(KParams kp, const double* __restrict__ q, double* __restrict__ face,
-                      int tile_x0, int tile_y0, int tile_z0) {
-    using FS = FaceSplit<P, DIM, AXIS>;
-    constexpr int NC = FS::NC, PG = FS::PG, NT = FS::NT;
-    constexpr int C1 = (AXIS + 1) % 3, C2 = (AXIS + 2) % 3;
-    extern __shared__ double smem[];
-    double* sc = smem;                  // staging [2][NC][32]
-    double* xs = smem;                  // after B1: [2][30][PG][32]
-    double* ys = smem + 2 * 30 * PG * 32;  // [2][10][PG][32]
-    double* ps = smem + (FS::STAGE > FS::XY ? FS::STAGE : FS::XY);  // [2][PG][32]
-
-    const int tid = threadIdx.x;
-    const int bx = blockIdx.x + tile_x0 * FS::NGRP;
-    const int grp = bx % FS::NGRP;
-    const int i0 = (bx / FS::NGRP) * 32;
-    const int j = blockIdx.y + tile_y0;
-    const int k = blockIdx.z + tile_z0;
-    const int nx = kp.nx, ny = kp.ny;
-
-    for (int e = tid; e < 2 * NC * 32; e += NT) {
-        const int l = e & 31;
-        const int row = e >> 5;
-        const int side = row >= NC;
-        const int comp = row - side * NC;
-        const int i = i0 + l;
-        double v = 0.0;
-        if (i < nx) {
-            int ci = i, cj = j, ck = k;
-            if (!side) {
-                if (AXIS == 0) ci = (i == 0 ? nx - 1 : i - 1);
-                if (AXIS == 1) cj = (j == 0 ? ny - 1 : j - 1);
-                if (AXIS == 2) ck = k - 1;
-            }
-            v = __ldg(q + comp * kp.cs + (long)(ck + 1) * kp.S + (long)cj * nx + ci);
-        }
-        sc[(side * NC + comp) * 32 + l] = v;
-    }
-    __syncthreads();  // B0
-
-    const int lane = tid & 31;
-    const int w = tid >> 5;
-    const int side = w / PG, pl = w - side * PG;
-    const int p = grp * PG + pl;
-    const int i = i0 + lane;
-    const bool valid = i < nx;
-    const int ic = valid ? i : nx - 1;  // clamp so invalid lanes run harmless code
-
-    // this side's cell: side 0 = minus-side neighbour, 1 = the face's own cell
-    const int ci = (side == 0 && AXIS == 0) ? (ic == 0 ? nx - 1 : ic - 1) : ic;
-    const int cj = (side == 0 && AXIS == 1) ? (j == 0 ? ny - 1 : j - 1) : j;
-    const int ck = (side == 0 && AXIS == 2) ? k - 1 : k;
-    const double i2h[3] = {__ldg(kp.i2dx + ci), __ldg(kp.i2dy + cj), __ldg(kp.i2dz + ck + 1)};
-    double t[20];
-    face_trace_rt<P, DIM, AXIS, FS::NFP>(p, side, sc + side * NC * 32 + lane, i2h, t);
-    ps[(side * PG + pl) * 32 + lane] = pressure_q(t, kp.gas);
-    __syncthreads();  // B1: traces done (staging dead), pressures visible
-
-    double tau = 0.0, rh = 0.0;
-    if (VISC) {  // tau = mu / mean trace pressure (dg.hpp:378-383), same order on both sides
-        const double psum = ps[pl * 32 + lane] + ps[(PG + pl) * 32 + lane];
-        tau = kp.two_mu / psum;
-        rh = psum * kp.rh_coef;
-    }
-    const TimeW tw = time_weights_r(tau, kp.inv_dt, rh);
-    const bool owned = k < kp.nzl;
-    const long item = (long)AXIS * kp.ncells_glob + (long)i + (long)nx * (j + (long)ny * (k + kp.kglob0));
-
-    SmemAcc acc{xs + (side * 30 * PG + pl) * 32 + lane, PG * 32};
-    flux_init(acc);
-    double bad = 0.0;
-    int rc = flux_side<VISC>(t, side, kp.gas, tw, acc, bad);
-    if (rc && valid && owned) report_error(kp, err_key(kp.stage, 0, item, p, side, rc), bad);
-    __syncthreads();  // B2: both sides' contributions visible
-
-    double q0[5], dq0[15];
-    const double* x0 = xs + pl * 32 + lane;
-    const double* x1 = xs + (30 * PG + pl) * 32 + lane;
-#pragma unroll
-    for (int m = 0; m < 5; ++m) q0[m] = x0[m * PG * 32] + x1[m * PG * 32];
-#pragma unroll
-    for (int m = 0; m < 15; ++m) dq0[m] = x0[(5 + m) * PG * 32] + x1[(5 + m) * PG * 32];
-    MergeState M;
-    double Fp[5], Ftp[5];
-    rc = merge_setup(kp.gas, q0, dq0, M, bad);
-    if (rc) {
-        if (side == 0 && valid && owned) report_error(kp, err_key(kp.stage, 0, item, p, 2, rc), bad);
-#pragma unroll
-        for (int m = 0; m < 5; ++m) Fp[m] = Ftp[m] = 0.0;
-    } else if (side == 0) {
-        merge_part_a(M, tw, Fp, Ftp);
-    } else {
-        merge_part_b<VISC>(M, tw, Fp, Ftp);
-    }
-    double* y = ys + (side * 10 * PG + pl) * 32 + lane;
-#pragma unroll
-    for (int m = 0; m < 5; ++m) {
-        y[m * PG * 32] = Fp[m];
-        y[(5 + m) * PG * 32] = Ftp[m];
-    }
-    __syncthreads();  // B3
-    if (!valid || kp.report) return;
-    // side 0 writes F, side 1 writes Ft: neq_L + neq_R + eqA + eqB (fixed order)
-    const double* y0 = ys + pl * 32 + lane;
-    const double* y1 = ys + (10 * PG + pl) * 32 + lane;
-    const int o = side * 5;
-    double Fl[5];
-#pragma unroll
-    for (int m = 0; m < 5; ++m)
-        Fl[m] = (x0[(20 + o + m) * PG * 32] + x1[(20 + o + m) * PG * 32]) +
-                (y0[(o + m) * PG * 32] + y1[(o + m) * PG * 32]);
-    // face-local -> global (dg.hpp:336-345)
-    double G[5];
-    G[0] = Fl[0];
-    G[4] = Fl[4];
-    G[1 + AXIS] = Fl[1];
-    G[1 + C1] = Fl[2];
-    G[1 + C2] = Fl[3];
-    const long fidx = (long)i + (long)nx * (j + (long)ny * k);
-    double* out = face + (long)(p * 10 + o) * kp.fs + fidx;
-#pragma unroll
-    for (int v = 0; v < 5; ++v) out[v * kp.fs] = G[v];
-    if (kp.count_fluxes && owned && side == 0) atomicAdd(kp.flux_count, 1ull);
 }
 
 // -------------------------------------------------------------- cell kernel

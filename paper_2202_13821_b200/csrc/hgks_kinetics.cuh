@@ -265,27 +265,17 @@ HD TimeW time_weights(double tau, double dt) {
 // time: F and dF/dt at t_n (flux.hpp:71-124 + :180-189), split into one pass
 // per side plus a merge so a kernel can build each trace just in time.
 // Traces are in the face-local frame: q[5], dq_n[5], dq_t1[5], dq_t2[5].
-// The 30-double accumulator that lives across the passes is reached through
-// an accessor: registers (FluxAcc) or a per-thread shared-memory column
-// (SmemAcc, frees ~60 registers in the face kernel).
+// A side pass accumulates its half-space moments of the merged state and
+// slopes and its UNWEIGHTED non-equilibrium moments, and reports its pressure:
+// tau = mu / mean trace pressure (dg.hpp:378-383) needs both sides, so the
+// time weights enter once, in the merge.
 struct FluxAcc {
-    double q0_[5];      // rho_l <psi>_+ + rho_r <psi>_-        (flux.hpp:85-86)
-    double dq0_[3][5];  // rho_l <a_l psi>_+ + rho_r <a_r psi>_- (flux.hpp:92-93)
-    double F_[5], Ft_[5];
+    double q0_[5];      // rho_l <psi>_+ + rho_r <psi>_-              (flux.hpp:85-86)
+    double dq0_[3][5];  // rho_l <a_l psi>_+ + rho_r <a_r psi>_-       (flux.hpp:92-93)
+    double nq_[3][5];   // sum_sides rho <u psi>_h, <u (a.u) psi>_h, <u A psi>_h (flux.hpp:112-121)
     HD double& q0(int m) { return q0_[m]; }
     HD double& dq0(int d, int m) { return dq0_[d][m]; }
-    HD double& F(int m) { return F_[m]; }
-    HD double& Ft(int m) { return Ft_[m]; }
-};
-
-// [slot][thread] layout: consecutive lanes hit consecutive 8-byte words
-struct SmemAcc {
-    double* p;   // &base[tid]
-    int stride;  // threads per CTA
-    HD double& q0(int m) { return p[m * stride]; }
-    HD double& dq0(int d, int m) { return p[(5 + 5 * d + m) * stride]; }
-    HD double& F(int m) { return p[(20 + m) * stride]; }
-    HD double& Ft(int m) { return p[(25 + m) * stride]; }
+    HD double& nq(int k, int m) { return nq_[k][m]; }
 };
 
 template <class Acc>
@@ -293,20 +283,11 @@ HD void flux_init(Acc& acc) {
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
         acc.q0(m) = 0.0;
-        acc.dq0(0, m) = 0.0;
-        acc.dq0(1, m) = 0.0;
-        acc.dq0(2, m) = 0.0;
-        acc.F(m) = 0.0;
-        acc.Ft(m) = 0.0;
-    }
-}
-
-template <class Acc>
-HD void acc_flux(Acc& acc, double sF, double sFt, const double* r) {
 #pragma unroll
-    for (int m = 0; m < 5; ++m) {
-        acc.F(m) += sF * r[m];
-        acc.Ft(m) += sFt * r[m];
+        for (int d = 0; d < 3; ++d) {
+            acc.dq0(d, m) = 0.0;
+            acc.nq(d, m) = 0.0;
+        }
     }
 }
 
@@ -323,13 +304,14 @@ HD void directional_flux(const double* Ut, const T& t, const Slope* a, double* o
     for (int m = 0; m < 5; ++m) out[m] += r[m];
 }
 
-// side 0 = left (u>0 half), 1 = right (u<0 half). Returns ERR_*.
+// side 0 = left (u>0 half), 1 = right (u<0 half). Returns ERR_*; p_side is the
+// trace pressure (core.hpp:72-74) for tau.
 template <bool VISCOUS, class Acc>
-HD int flux_side(const double* t, int side, const GasC& g, const TimeW& tw, Acc& acc,
-                 double& bad) {
+HD int flux_side(const double* t, int side, const GasC& g, Acc& acc, double& p_side, double& bad) {
     Prim w;
     const int rc = prim_from_q(t, g, w, bad);
     if (rc) return rc;
+    p_side = w.rho * w.il;
     const SolveC sc = solve_consts(w, g);
     Tab<6, 5> tb;  // U: half table (orders 0..6); V, W full
     const double il = w.il;
@@ -363,53 +345,17 @@ HD int flux_side(const double* t, int side, const GasC& g, const TimeW& tw, Acc&
         tf.xi2 = tb.xi2;
         tf.dxi = tb.dxi;
         const Slope A = time_coefficient(sc, tf, a);
-        // free-streaming terms of this side (flux.hpp:112-121)
+        // free-streaming moments of this side (flux.hpp:112-121), unweighted
         psi_moment<1, 0, 0>(tb.U, tb, r);
-        acc_flux(acc, w.rho * tw.f0F, w.rho * tw.f0Ft, r);
+#pragma unroll
+        for (int m = 0; m < 5; ++m) acc.nq(0, m) += w.rho * r[m];
         directional_flux(tb.U, tb, a, r);
-        acc_flux(acc, w.rho * tw.anF, w.rho * tw.anFt, r);
+#pragma unroll
+        for (int m = 0; m < 5; ++m) acc.nq(1, m) += w.rho * r[m];
         slope_moment<1, 0, 0>(tb.U, tb, A, r);
-        acc_flux(acc, w.rho * tw.AnF, w.rho * tw.AnFt, r);
-    }
-    return ERR_NONE;
-}
-
-// equilibrium part from the merged state (flux.hpp:87-106); F/Ft final after.
-template <bool VISCOUS, class Acc>
-HD int flux_merge(const GasC& g, const TimeW& tw, Acc& acc, double& bad) {
-    Prim w0;
-    double q0[5];
 #pragma unroll
-    for (int m = 0; m < 5; ++m) q0[m] = acc.q0(m);
-    const int rc = prim_from_q(q0, g, w0, bad);
-    if (rc) return rc;
-    const SolveC s0 = solve_consts(w0, g);
-    Tab<6, 5> t0;
-    const double il = w0.il;
-    full_seq<6>(w0.U, il, t0.U);
-    full_seq<5>(w0.V, il, t0.V);
-    full_seq<5>(w0.W, il, t0.W);
-    t0.xi2 = g.K * il;
-    t0.dxi = 2.0 * g.K * il * il;
-    Slope ab[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        double dq[5];
-#pragma unroll
-        for (int m = 0; m < 5; ++m) dq[m] = acc.dq0(d, m);
-        ab[d] = micro_slope(s0, w0.inv_rho, dq);
+        for (int m = 0; m < 5; ++m) acc.nq(2, m) += w.rho * r[m];
     }
-    const Slope Ab = time_coefficient(s0, t0, ab);
-    double r[5];
-    psi_moment<1, 0, 0>(t0.U, t0, r);
-    acc_flux(acc, w0.rho * tw.g0F, w0.rho * tw.g0Ft, r);
-    // abar's weight vanishes at tau = 0 (flux.hpp:32-37)
-    if (VISCOUS) {
-        directional_flux(t0.U, t0, ab, r);
-        acc_flux(acc, w0.rho * tw.abF, w0.rho * tw.abFt, r);
-    }
-    slope_moment<1, 0, 0>(t0.U, t0, Ab, r);
-    acc_flux(acc, w0.rho * tw.AbF, w0.rho * tw.AbFt, r);
     return ERR_NONE;
 }
 
@@ -475,32 +421,57 @@ HD void merge_part_b(const MergeState& M, const TimeW& tw, double* F, double* Ft
     }
 }
 
-// Whole interface flux from two traces; stage = 0 left, 1 right, 2 merged on
-// failure (the reference's check order, flux.hpp:73-87).
+// Merged-state equilibrium terms (flux.hpp:87-106) plus the time-weighted
+// non-equilibrium moments (flux.hpp:112-121): F, Ft final.
+template <bool VISCOUS, class Acc>
+HD int flux_merge(const GasC& g, const TimeW& tw, Acc& acc, double* F, double* Ft, double& bad) {
+    double q0[5], dq0[15];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+        q0[m] = acc.q0(m);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) dq0[5 * d + m] = acc.dq0(d, m);
+    }
+    MergeState M;
+    const int rc = merge_setup(g, q0, dq0, M, bad);
+    if (rc) return rc;
+    merge_part_a(M, tw, F, Ft);
+    double Fb[5], Ftb[5];
+    merge_part_b<VISCOUS>(M, tw, Fb, Ftb);
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+        F[m] += Fb[m];
+        Ft[m] += Ftb[m];
+        if (VISCOUS) {
+            F[m] += tw.f0F * acc.nq(0, m) + tw.anF * acc.nq(1, m) + tw.AnF * acc.nq(2, m);
+            Ft[m] += tw.f0Ft * acc.nq(0, m) + tw.anFt * acc.nq(1, m) + tw.AnFt * acc.nq(2, m);
+        }
+    }
+    return ERR_NONE;
+}
+
+// Whole interface flux from two traces at a given tau; stage = 0 left,
+// 1 right, 2 merged on failure (the reference's check order, flux.hpp:73-87).
 template <bool VISCOUS>
 HD int interface_flux(const double* tl, const double* tr, const GasC& g, const TimeW& tw,
                       double* F, double* Ft, int& stage, double& bad) {
     FluxAcc acc;
     flux_init(acc);
-    int rc = flux_side<VISCOUS>(tl, 0, g, tw, acc, bad);
+    double pl = 0.0, pr = 0.0;
+    int rc = flux_side<VISCOUS>(tl, 0, g, acc, pl, bad);
     if (rc) {
         stage = 0;
         return rc;
     }
-    rc = flux_side<VISCOUS>(tr, 1, g, tw, acc, bad);
+    rc = flux_side<VISCOUS>(tr, 1, g, acc, pr, bad);
     if (rc) {
         stage = 1;
         return rc;
     }
-    rc = flux_merge<VISCOUS>(g, tw, acc, bad);
+    rc = flux_merge<VISCOUS>(g, tw, acc, F, Ft, bad);
     if (rc) {
         stage = 2;
         return rc;
-    }
-#pragma unroll
-    for (int m = 0; m < 5; ++m) {
-        F[m] = acc.F(m);
-        Ft[m] = acc.Ft(m);
     }
     return ERR_NONE;
 }
