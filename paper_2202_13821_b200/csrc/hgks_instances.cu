@@ -47,7 +47,8 @@ struct Launch {
             count = 1;
             grid = 1;
         }
-        face_kernel<P, DIM, VISC, AXIS><<<grid, 32 * NFP, face_smem<AXIS>(), st>>>(kp, q, f, first, count, 0);
+        (void)NFP;
+        face_kernel<P, DIM, VISC, AXIS><<<grid, FaceCTA<P, DIM, AXIS>::NT, face_smem<AXIS>(), st>>>(kp, q, f, first, count, 0);
     }
     static void face(const KParams& kp, const double* q, double* const f[3], cudaStream_t st,
                      int report, const int* tile) {
@@ -106,8 +107,7 @@ struct Launch {
         const void* ffn[3] = {(const void*)face_kernel<P, DIM, VISC, 0>,
                               (const void*)face_kernel<P, DIM, VISC, 1>,
                               (const void*)face_kernel<P, DIM, VISC, 2>};
-        const int fnt[3] = {32 * SH::template nfp<0>(), 32 * SH::template nfp<1>(),
-                            32 * SH::template nfp<2>()};
+        const int fnt[3] = {FaceCTA<P, DIM, 0>::NT, FaceCTA<P, DIM, 1>::NT, FaceCTA<P, DIM, 2>::NT};
         const int fsm[3] = {face_smem<0>(), face_smem<1>(), face_smem<2>()};
         for (int a = 0; a < 3 && e == cudaSuccess; ++a) {
             int nb = 0;

@@ -192,14 +192,23 @@ __device__ __forceinline__ void cp_async_wait() {
 // NEXT tile stream into the other half of a double-buffered shared-memory
 // stage [2][side][comp][32] (cp.async, coalesced 256 B rows) while the
 // current tile's fluxes are computed.
+// P3 (9 points) runs 3 points per warp so its 3-warp CTAs can hold 255 registers.
+template <int P, int DIM, int AXIS>
+struct FaceCTA {
+    static constexpr int NFP = Shape<P, DIM>::template nfp<AXIS>();
+    static constexpr int PPW = (P == 3 && NFP % 3 == 0) ? 3 : 1;  // points per warp
+    static constexpr int NT = 32 * NFP / PPW;
+};
+
 template <int P, int DIM, bool VISC, int AXIS>
-__global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>(), HGKS_FACE_MINB_P(P))
+__global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_P(P))
     face_kernel(KParams kp, const double* __restrict__ q, double* __restrict__ face,
                 int tile_first, int tile_count, int unused) {
     using SH = Shape<P, DIM>;
     constexpr int NC = SH::NC;
     constexpr int NFP = SH::template nfp<AXIS>();
-    constexpr int NT = 32 * NFP;
+    constexpr int PPW = FaceCTA<P, DIM, AXIS>::PPW;
+    constexpr int NT = FaceCTA<P, DIM, AXIS>::NT;
     constexpr int C1 = (AXIS + 1) % 3, C2 = (AXIS + 2) % 3;
     constexpr int STG = 2 * NC * 32;  // one stage: [side][comp][32]
     extern __shared__ double smem[];
@@ -230,7 +239,7 @@ __global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>(), HGKS
     };
 
     const int lane = tid & 31;
-    const int p = tid >> 5;
+    const int warp = tid >> 5;
     const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
     if (t0 < tile_end) prefetch(t0, smem);
     cp_async_commit();
@@ -243,6 +252,9 @@ __global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>(), HGKS
         const int i = i0 + lane;
         cp_async_wait<1>();  // this tile's stage
         __syncthreads();
+#pragma unroll 1
+        for (int ip = 0; ip < PPW; ++ip) {
+        const int p = warp * PPW + ip;
         if (i < nx) {
             const int im = AXIS == 0 ? (i == 0 ? nx - 1 : i - 1) : i;
             const int jm = AXIS == 1 ? (j == 0 ? ny - 1 : j - 1) : j;
@@ -305,6 +317,7 @@ __global__ void __launch_bounds__(32 * Shape<P, DIM>::template nfp<AXIS>(), HGKS
                 if (kp.count_fluxes && owned) atomicAdd(kp.flux_count, 1ull);
             }
         }
+        }  // points of this warp
         __syncthreads();  // this stage is free for the prefetch two tiles ahead
     }
     cp_async_wait<0>();
