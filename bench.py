@@ -235,22 +235,25 @@ def main():
         q_pin = torch.empty(s.ncoeffs, dtype=torch.float64, pin_memory=True)
         q = q_pin.numpy()
         q[:], _ = s.get_state()
+        nch = 16 if world == 1 else 1  # the streamed step pipelines a single slab
         for _ in range(2):
-            s.two_stage_step_host(q, s.compute_dt(cfl))
+            s.two_stage_step_host_streamed(q, s.compute_dt(cfl), nch)
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         k2 = max(3, min(a.steps, 10))
         t0 = time.perf_counter()
         for _ in range(k2):
-            s.two_stage_step_host(q, s.compute_dt(cfl))  # H2D, step, D2H (synchronous)
+            # H2D of the state, step, D2H of the state; z-chunked so the copies
+            # overlap the kernels; synchronous per call
+            s.two_stage_step_host_streamed(q, s.compute_dt(cfl), nch)
         el2 = time.perf_counter() - t0
         t2 = torch.tensor([el2], dtype=torch.float64, device=dev)
         if world > 1:
             torch.distributed.all_reduce(t2, op=torch.distributed.ReduceOp.MAX)
         e2e = {"value": dof_glob * k2 / float(t2.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(s.ncoeffs * 8), "d2h_bytes_per_step": int(s.ncoeffs * 8),
-               "steps": k2, "path": "hgks_two_stage_step_host (pinned host AoS state)"}
+               "steps": k2, "path": f"hgks_two_stage_step_host_streamed (pinned host AoS state, {nch} z-chunks)"}
 
     if rank != 0:
         if world > 1:

@@ -94,6 +94,14 @@ int hgks_step(hgks_solver* s, double dt);
  * two_stage_step(r.state.coeffs, dt, eval, scratch). */
 int hgks_two_stage_step_host(hgks_solver* s, double* q, double dt);
 
+/* The same step with the host<->device traffic streamed: the z range is cut
+ * into `nchunks` slabs whose uploads, face/cell kernels (a z-wavefront) and
+ * downloads overlap on three streams. Results are bitwise identical to
+ * hgks_two_stage_step_host. Difference: on a state error q may already hold
+ * some advanced chunks (the device state is unchanged). Single slab only;
+ * otherwise it falls back to hgks_two_stage_step_host. */
+int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int nchunks);
+
 /* advance() (solver.hpp:62-108) without records: steps from the current time
  * to t_end with dt = compute_dt (cfl) or dt_fixed (> 0), clipped to t_end and
  * to multiples of record_interval (> 0 only). Writes the number of steps taken. */

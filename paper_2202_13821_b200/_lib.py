@@ -25,7 +25,7 @@ EXPORTS = [
     "hgks_abi_version", "hgks_create", "hgks_destroy", "hgks_last_error", "hgks_error_info",
     "hgks_num_basis", "hgks_num_coeffs", "hgks_face_points", "hgks_set_state", "hgks_get_state",
     "hgks_residual", "hgks_apply_inverse_mass", "hgks_compute_dt", "hgks_step",
-    "hgks_two_stage_step_host", "hgks_advance", "hgks_set_count_fluxes", "hgks_flux_evaluations",
+    "hgks_two_stage_step_host", "hgks_two_stage_step_host_streamed", "hgks_advance", "hgks_set_count_fluxes", "hgks_flux_evaluations",
     "hgks_project_case", "hgks_tgv_diagnostics", "hgks_error_norms", "hgks_halo_bytes", "hgks_halo_buffers",
     "hgks_halo_pack", "hgks_halo_unpack", "hgks_set_halo_exchange", "hgks_step_phase",
     "hgks_set_dt_reduce", "hgks_set_stream", "hgks_get_stream", "hgks_synchronize",
@@ -79,6 +79,7 @@ def load():
     L.hgks_compute_dt.argtypes = [sp, ctypes.c_double, _dp]
     L.hgks_step.argtypes = [sp, ctypes.c_double]
     L.hgks_two_stage_step_host.argtypes = [sp, _dp, ctypes.c_double]
+    L.hgks_two_stage_step_host_streamed.argtypes = [sp, _dp, ctypes.c_double, ctypes.c_int]
     L.hgks_advance.argtypes = [sp, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, _ip]
     L.hgks_set_count_fluxes.argtypes = [sp, ctypes.c_int]
     L.hgks_set_count_fluxes.restype = None

@@ -9,11 +9,12 @@ namespace hgks_dev {
 
 // host AoS [(c*NC) + comp] (owned cells) <-> device SoA comp*cs + S + c.
 // 32 cells per block, staged through shared memory so both sides coalesce.
+// cells [cbeg, cend) of the owned range (cend < 0: all)
 __global__ void aos_to_soa_kernel(KParams kp, const double* __restrict__ aos,
-                                  double* __restrict__ soa, int NC) {
+                                  double* __restrict__ soa, int NC, long cbeg = 0, long cend = -1) {
     __shared__ double st[100 * 33];
-    const long ncell = (long)kp.S * kp.nzl;
-    for (long c0 = (long)blockIdx.x * 32; c0 < ncell; c0 += (long)gridDim.x * 32) {
+    const long ncell = cend < 0 ? (long)kp.S * kp.nzl : cend;
+    for (long c0 = cbeg + (long)blockIdx.x * 32; c0 < ncell; c0 += (long)gridDim.x * 32) {
         const int nc = (int)min(32L, ncell - c0);
         for (int e = threadIdx.x; e < nc * NC; e += blockDim.x) {
             const int l = e / NC, comp = e - l * NC;
@@ -29,10 +30,10 @@ __global__ void aos_to_soa_kernel(KParams kp, const double* __restrict__ aos,
 }
 
 __global__ void soa_to_aos_kernel(KParams kp, const double* __restrict__ soa,
-                                  double* __restrict__ aos, int NC) {
+                                  double* __restrict__ aos, int NC, long cbeg = 0, long cend = -1) {
     __shared__ double st[100 * 33];
-    const long ncell = (long)kp.S * kp.nzl;
-    for (long c0 = (long)blockIdx.x * 32; c0 < ncell; c0 += (long)gridDim.x * 32) {
+    const long ncell = cend < 0 ? (long)kp.S * kp.nzl : cend;
+    for (long c0 = cbeg + (long)blockIdx.x * 32; c0 < ncell; c0 += (long)gridDim.x * 32) {
         const int nc = (int)min(32L, ncell - c0);
         for (int e = threadIdx.x; e < 32 * NC; e += blockDim.x) {
             const int l = e & 31, comp = e >> 5;

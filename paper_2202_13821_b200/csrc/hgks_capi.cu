@@ -45,7 +45,10 @@ struct hgks_solver {
     // device memory
     double *d_tab = nullptr, *d_dx = nullptr, *d_dy = nullptr, *d_dz = nullptr;
     double *qa = nullptr, *qb = nullptr, *qs = nullptr, *L1 = nullptr, *Lt1 = nullptr;
-    double *R = nullptr, *Rt = nullptr, *tmp = nullptr;
+    double *R = nullptr, *Rt = nullptr, *tmp = nullptr, *tmp2 = nullptr;
+    // streamed host step: copy streams and per-chunk events
+    cudaStream_t st_up = nullptr, st_dn = nullptr;
+    std::vector<cudaEvent_t> ev_up, ev_c2, ev_dn;
     double* face[3] = {nullptr, nullptr, nullptr};
     unsigned long long* d_key = nullptr;  // [0] error key, [1] dt bits, [2] flux count
     double* d_val = nullptr;
@@ -393,11 +396,16 @@ int hgks_create(const hgks_config* cfg, hgks_solver** out) {
 void hgks_destroy(hgks_solver* s) {
     if (!s) return;
     for (double* p : {s->d_tab, s->d_dx, s->d_dy, s->d_dz, s->qa, s->qb, s->qs, s->L1, s->Lt1,
-                      s->R, s->Rt, s->tmp, s->face[0], s->face[1], s->face[2], s->d_val, s->d_red, s->d_halo})
+                      s->R, s->Rt, s->tmp, s->tmp2, s->face[0], s->face[1], s->face[2], s->d_val, s->d_red,
+                      s->d_halo})
         if (p) cudaFree(p);
     if (s->d_key) cudaFree(s->d_key);
     for (auto& e : s->ev)
         if (e) cudaEventDestroy(e);
+    for (auto* v : {&s->ev_up, &s->ev_c2, &s->ev_dn})
+        for (auto e : *v) cudaEventDestroy(e);
+    if (s->st_up) cudaStreamDestroy(s->st_up);
+    if (s->st_dn) cudaStreamDestroy(s->st_dn);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
 }
@@ -596,6 +604,118 @@ int hgks_two_stage_step_host(hgks_solver* s, double* q, double dt) {
     rc = do_step(s, dt);
     if (rc) return rc;
     return download_aos(s, s->qa, q);
+}
+
+int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int nchunks) {
+    // Streamed S2O4 step on a host vector. The z range is cut into chunks; the
+    // H2D copies, a z-wavefront of face/cell kernels and the D2H copies run on
+    // three streams so transfers overlap compute:
+    //   uploads (copy stream):  U(N-1), U(0), U(1), ..., U(N-2)
+    //   compute (solver stream): ghost(q^n), F1(0); for i: F1(i+1), C1(i),
+    //            F2(i) (i >= 1), C2(i-1) (i-1 >= 1); then ghost(q*), F2(0),
+    //            C2(N-1), C2(0)      (periodic z: chunk 0's stage 2 needs the
+    //            last chunk's q*, so it closes the wavefront)
+    //   downloads (copy stream): D(1), ..., D(N-1), D(0) after their C2.
+    // Stage 1 of chunk c needs U(c-1..c+1); its stage 2 needs C1(c-1..c+1).
+    if (!s->single || nchunks <= 1 || s->nzl < 4) return hgks_two_stage_step_host(s, q, dt);
+    const int N = std::min(nchunks, s->nzl / 2);
+    int rc = ensure_tmp(s);
+    if (rc) return rc;
+    const size_t arr = (size_t)s->NC * s->cs * sizeof(double);
+    if (!s->tmp2) CK(cudaMalloc(&s->tmp2, arr));
+    if (!s->st_up) CK(cudaStreamCreateWithFlags(&s->st_up, cudaStreamNonBlocking));
+    if (!s->st_dn) CK(cudaStreamCreateWithFlags(&s->st_dn, cudaStreamNonBlocking));
+    while ((int)s->ev_up.size() < N) {
+        cudaEvent_t a, b, c;
+        CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
+        s->ev_up.push_back(a);
+        s->ev_c2.push_back(b);
+        s->ev_dn.push_back(c);
+    }
+    auto kb = [&](int c) { return (int)((long)c * s->nzl / N); };
+    const long S = s->S;
+    const int NC = s->NC;
+    KParams kp0 = make_params(s, 0.0, 0);
+    const int tblocks = 148 * 8;
+    // the previous call's downloads must be done before tmp2 / q are reused
+    CK(cudaStreamSynchronize(s->st_dn));
+    rc = reset_error(s);
+    if (rc) return rc;
+    // ---- uploads
+    cudaEvent_t start;
+    CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    CK(cudaEventRecord(start, s->stream));  // after reset_error on the compute stream
+    CK(cudaStreamWaitEvent(s->st_up, start, 0));
+    for (int u = 0; u < N; ++u) {
+        const int c = u == 0 ? N - 1 : u - 1;
+        const long c0 = kb(c) * S, c1 = kb(c + 1) * S;
+        CK(cudaMemcpyAsync(s->tmp + c0 * NC, q + c0 * NC, (size_t)(c1 - c0) * NC * sizeof(double),
+                           cudaMemcpyHostToDevice, s->st_up));
+        aos_to_soa_kernel<<<tblocks, 256, 0, s->st_up>>>(kp0, s->tmp, s->qa, NC, c0, c1);
+        ++s->launches;
+        CK(cudaEventRecord(s->ev_up[c], s->st_up));
+    }
+    cudaEventDestroy(start);
+    // ---- compute wavefront
+    const KParams kp1 = make_params(s, dt, 0), kp2 = make_params(s, dt, 1);
+    const KernelSet& K = s->ks;
+    cudaStream_t cs = s->stream;
+    auto wait_up = [&](int c) { return cudaStreamWaitEvent(cs, s->ev_up[(c + N) % N], 0); };
+    auto F1 = [&](int c) { K.face_layers(kp1, s->qa, s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
+    auto C1 = [&](int c) {
+        K.cell_layers(kp1, MODE_STAGE1, s->qa, s->face, nullptr, nullptr, nullptr, s->qs, s->L1, s->Lt1, cs,
+                      kb(c), kb(c + 1));
+        ++s->launches;
+    };
+    auto F2 = [&](int c) { K.face_layers(kp2, s->qs, s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
+    auto C2 = [&](int c) {
+        K.cell_layers(kp2, MODE_STAGE2, s->qs, s->face, s->qa, s->L1, s->Lt1, s->qb, nullptr, nullptr, cs,
+                      kb(c), kb(c + 1));
+        ++s->launches;
+        return cudaEventRecord(s->ev_c2[c], cs);
+    };
+    auto ghost = [&](double* a) {
+        ghost_wrap_kernel<<<148 * 4, 256, 0, cs>>>(kp0, a, NC);
+        ++s->launches;
+    };
+    CK(wait_up(N - 1));
+    CK(wait_up(0));
+    ghost(s->qa);
+    F1(0);
+    for (int i = 0; i < N; ++i) {
+        if (i + 1 <= N - 1) {
+            CK(wait_up(i + 1));
+            F1(i + 1);
+        }
+        C1(i);
+        if (i >= 1) F2(i);
+        if (i - 1 >= 1) CK(C2(i - 1));
+    }
+    ghost(s->qs);
+    F2(0);
+    CK(C2(N - 1));
+    CK(C2(0));
+    CK(cudaGetLastError());
+    // ---- downloads in completion order
+    for (int d = 0; d < N; ++d) {
+        const int c = d == N - 1 ? 0 : d + 1;
+        const long c0 = kb(c) * S, c1 = kb(c + 1) * S;
+        CK(cudaStreamWaitEvent(s->st_dn, s->ev_c2[c], 0));
+        soa_to_aos_kernel<<<tblocks, 256, 0, s->st_dn>>>(kp0, s->qb, s->tmp2, NC, c0, c1);
+        ++s->launches;
+        CK(cudaMemcpyAsync(q + c0 * NC, s->tmp2 + c0 * NC, (size_t)(c1 - c0) * NC * sizeof(double),
+                           cudaMemcpyDeviceToHost, s->st_dn));
+    }
+    CK(cudaStreamSynchronize(s->st_dn));
+    const double* inputs[2] = {s->qa, s->qs};
+    bool failed = false;
+    rc = check_error(s, inputs, dt, &failed);
+    if (rc) return rc;  // q holds a partially advanced state (documented in the header)
+    std::swap(s->qa, s->qb);
+    s->time += dt;
+    return HGKS_OK;
 }
 
 int hgks_advance(hgks_solver* s, double t_end, double cfl, double dt_fixed, double record_interval,

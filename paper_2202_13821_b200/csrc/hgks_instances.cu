@@ -50,6 +50,37 @@ struct Launch {
         (void)NFP;
         face_kernel<P, DIM, VISC, AXIS><<<grid, FaceCTA<P, DIM, AXIS>::NT, face_smem<AXIS>(), st>>>(kp, q, f, first, count, 0);
     }
+    template <int AXIS>
+    static void face_axis_layers(const KParams& kp, const double* q, double* f, cudaStream_t st,
+                                 int kb, int ke) {
+        const int ntx = (kp.nx + 31) / 32;
+        const int first = ntx * kp.ny * kb, count = ntx * kp.ny * (ke - kb);
+        if (count <= 0) return;
+        const int grid = std::min(count, std::max(1, face_grid[AXIS]));
+        face_kernel<P, DIM, VISC, AXIS><<<grid, FaceCTA<P, DIM, AXIS>::NT, face_smem<AXIS>(), st>>>(
+            kp, q, f, first, count, 0);
+    }
+    static void face_layers(const KParams& kp, const double* q, double* const f[3], cudaStream_t st,
+                            int kb, int ke) {
+        face_axis_layers<0>(kp, q, f[0], st, kb, ke);
+        face_axis_layers<1>(kp, q, f[1], st, kb, ke);
+        face_axis_layers<2>(kp, q, f[2], st, kb, ke);
+    }
+    static void cell_layers(const KParams& kp, int mode, const double* qin, double* const f[3],
+                            const double* qn, const double* L1, const double* Lt1, double* o0,
+                            double* o1, double* o2, cudaStream_t st, int kb, int ke) {
+        const int ntx = (kp.nx + SH::TC - 1) / SH::TC;
+        const int first = ntx * kp.ny * kb, count = ntx * kp.ny * (ke - kb);
+        if (count <= 0) return;
+        const int grid = std::min(count, std::max(1, cell_grid[mode]));
+        const int smem = cell_smem();
+        if (mode == MODE_STAGE1)
+            cell_kernel<P, DIM, VISC, MODE_STAGE1><<<grid, SH::NT_CELL, smem, st>>>(
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
+        else
+            cell_kernel<P, DIM, VISC, MODE_STAGE2><<<grid, SH::NT_CELL, smem, st>>>(
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
+    }
     static void face(const KParams& kp, const double* q, double* const f[3], cudaStream_t st,
                      int report, const int* tile) {
         // report mode re-runs only the failing axis' tile (tile[3] = axis)
@@ -120,6 +151,8 @@ struct Launch {
         KernelSet k;
         k.face = &face;
         k.cell = &cell;
+        k.face_layers = &face_layers;
+        k.cell_layers = &cell_layers;
         k.face_smem[0] = face_smem<0>();
         k.face_smem[1] = face_smem<1>();
         k.face_smem[2] = face_smem<2>();

@@ -14,6 +14,13 @@ struct KernelSet {
     void (*cell)(const KParams&, int mode, const double* qin, double* const f[3], const double* qn,
                  const double* L1, const double* Lt1, double* o0, double* o1, double* o2,
                  cudaStream_t, int report, const int* tile);
+    // the same kernels restricted to owned z layers [kb, ke) (all three face
+    // axes / the cell update of those layers), for the streamed host step
+    void (*face_layers)(const KParams&, const double* q, double* const f[3], cudaStream_t, int kb,
+                        int ke);
+    void (*cell_layers)(const KParams&, int mode, const double* qin, double* const f[3],
+                        const double* qn, const double* L1, const double* Lt1, double* o0,
+                        double* o1, double* o2, cudaStream_t, int kb, int ke);
     int face_smem[3];
     int cell_smem;
     int cell_tc;

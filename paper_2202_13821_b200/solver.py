@@ -277,6 +277,13 @@ class Solver:
             raise ConfigError("q must be a contiguous float64 vector of the state size")
         self._check(self.L.hgks_two_stage_step_host(self.h, _ptr(q), dt))
 
+    def two_stage_step_host_streamed(self, q: np.ndarray, dt: float, nchunks: int = 16):
+        """The host-vector step with H2D / compute / D2H overlapped over z chunks
+        (bitwise identical results; on a state error q may be partially advanced)."""
+        if not (q.dtype == np.float64 and q.flags["C_CONTIGUOUS"] and q.size == self.ncoeffs):
+            raise ConfigError("q must be a contiguous float64 vector of the state size")
+        self._check(self.L.hgks_two_stage_step_host_streamed(self.h, _ptr(q), dt, nchunks))
+
     def advance_to(self, t_end: float, cfl: float, dt_fixed: float = 0.0, record_interval: float = 0.0) -> int:
         n = ctypes.c_int()
         self._check(self.L.hgks_advance(self.h, t_end, cfl, dt_fixed, record_interval, ctypes.byref(n)))

@@ -197,3 +197,25 @@ def test_tgv_diagnostics_match(hgks, oracle_mod):
     assert abs(rec.Ek - ek) <= 1e-13 * ek
     assert abs(rec.epsZeta - epsz) <= 1e-12 * epsz
     assert abs(rec.Ek - 0.125) <= 0.125 * 1e-3  # test_cases.cpp:140-150
+
+
+@pytest.mark.parametrize("case,n,degree,nchunks", [("tgv", 16, 2, 4), ("adv3d", 12, 2, 3), ("tgv", 8, 3, 4)])
+def test_streamed_host_step_bitwise(hgks, case, n, degree, nchunks):
+    """hgks_two_stage_step_host_streamed (chunked H2D / wavefront / D2H) gives
+    the same bits as the serial host step and the device-resident step."""
+    P = hgks
+    r = P.setup_run(P.CaseConfig.named(case, n), P.RunOptions(degree=degree))
+    q0 = r.solver.get_state()[0]
+    dts = []
+    qa = q0.copy()
+    for _ in range(3):
+        r.solver.set_state(qa)
+        dt = r.solver.compute_dt(P.default_cfl(degree))
+        dts.append(dt)
+        r.solver.two_stage_step_host(qa, dt)
+    qb = q0.copy()
+    r.solver.set_state(qb)
+    for dt in dts:
+        r.solver.two_stage_step_host_streamed(qb, dt, nchunks)
+    assert np.array_equal(qa, qb)
+    assert np.array_equal(r.solver.get_state()[0], qb)
