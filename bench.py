@@ -50,12 +50,14 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--case", default="tgv")
-    ap.add_argument("--n", type=int, default=128)
+    ap.add_argument("--mesh", dest="n", type=int, default=128)
     ap.add_argument("--degree", type=int, default=2)
     ap.add_argument("--cfl", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of CPU reference work")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo = host-staged halo exchange (multi-rank test mode on one GPU)")
     return ap.parse_args()
 
 
@@ -178,18 +180,29 @@ def main():
     import paper_2202_13821_b200 as P
     from paper_2202_13821_b200 import slabs
 
+    # HGKS_BENCH_DEVICE pins every rank to one GPU — only meaningful with
+    # --dist-backend gloo (host-staged halos), the mode that exercises the
+    # multi-rank path on a single-GPU box
+    if os.environ.get("HGKS_BENCH_DEVICE"):
+        local = int(os.environ["HGKS_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
+    coll_dev = "cpu" if a.dist_backend == "gloo" else dev  # where collectives' tensors live
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(dev))
+        if a.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(dev))
+        else:
+            dist.init_process_group("gloo")
     cfg = P.CaseConfig.named(a.case, a.n)
     opt = P.RunOptions(degree=a.degree, device=local)
     cfl = a.cfl or P.default_cfl(a.degree)
     zb, zc = slabs.slab_partition(a.n if cfg.dim == 3 else 1, world)[rank]
     r = P.setup_run(cfg, opt, z_begin=zb, z_count=zc if world > 1 else 0)
     s = r.solver
-    stream = torch.cuda.current_stream(local)
+    # one dedicated stream shared by the solver and torch (events, collectives)
+    stream = torch.cuda.Stream(local)
+    torch.cuda.set_stream(stream)
     s.set_stream(stream.cuda_stream)
     if world > 1:
         slabs.attach(s, rank, world, local)
@@ -223,7 +236,7 @@ def main():
         torch.distributed.barrier()
     launches = s.launch_count() - launches0
     el_ms = e0.elapsed_time(e1)
-    t = torch.tensor([el_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([el_ms], dtype=torch.float64, device=coll_dev)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     el_ms = float(t.item())
@@ -248,7 +261,7 @@ def main():
             # overlap the kernels; synchronous per call
             s.two_stage_step_host_streamed(q, s.compute_dt(cfl), nch)
         el2 = time.perf_counter() - t0
-        t2 = torch.tensor([el2], dtype=torch.float64, device=dev)
+        t2 = torch.tensor([el2], dtype=torch.float64, device=coll_dev)
         if world > 1:
             torch.distributed.all_reduce(t2, op=torch.distributed.ReduceOp.MAX)
         e2e = {"value": dof_glob * k2 / float(t2.item()), "unit": UNIT,
@@ -326,6 +339,7 @@ def main():
         "data": "synthetic: TGV Re=1600 Ma=0.1 initial field L2-projected on the device (no dataset)",
         "config": {"workload": workload(a), "case": a.case, "n": a.n, "degree": a.degree,
                    "cells": ncell_glob, "dof": dof_glob, "parallelism": f"z-slab x{world}",
+                   "halo_transport": a.dist_backend if world > 1 else None,
                    "l2": "inputs larger than L2 (state 839 MB at 128^3 P2); no flush"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -51,6 +51,11 @@ def device_view(ptr: int, nbytes: int, device: int):
     return torch.as_tensor(_CAI(), device=f"cuda:{device}")
 
 
+def torch_empty_like_cpu(t):
+    import torch
+    return torch.empty(t.shape, dtype=t.dtype)
+
+
 def exchange_halos(send_lo, send_hi, recv_lo, recv_hi, rank: int, world: int, group=None):
     """send_lo -> lower neighbour's recv_hi, send_hi -> upper neighbour's recv_lo.
 
@@ -62,6 +67,14 @@ def exchange_halos(send_lo, send_hi, recv_lo, recv_hi, rank: int, world: int, gr
     if world == 1:
         recv_hi.copy_(send_lo)
         recv_lo.copy_(send_hi)
+        return
+    if send_lo.is_cuda and dist.get_backend(group) == "gloo":
+        # host-staged exchange (gloo moves CPU tensors): the test mode that
+        # runs several ranks' solvers on one GPU without device-side waits
+        bufs = [t.cpu() for t in (send_lo, send_hi)] + [torch_empty_like_cpu(t) for t in (recv_lo, recv_hi)]
+        exchange_halos(bufs[0], bufs[1], bufs[2], bufs[3], rank, world, group)
+        recv_lo.copy_(bufs[2])
+        recv_hi.copy_(bufs[3])
         return
     lower, upper = ring_neighbors(rank, world)
     ops = [
@@ -102,13 +115,28 @@ def sum_allreduce(values, device: Optional[str] = None, group=None):
 def attach(solver, rank: int, world: int, device: int, group=None):
     """Wire a slab solver to torch.distributed: halo exchange on the solver's
     stream (which must be torch's current stream) and min-allreduce of dt."""
+    import torch
+
     nbytes = solver.halo_bytes()
     ptrs = solver.halo_buffers()
     views = [device_view(p, nbytes, device) for p in ptrs]
 
     def exchange(_s, _which):
+        # the pack kernel ran on the solver's stream; torch's copies / NCCL ops
+        # run on torch's current stream. When they are not the same stream,
+        # order them explicitly (stream 0 is the legacy default stream, never
+        # the solver's).
+        ts = torch.cuda.current_stream(device)
+        same = ts.cuda_stream != 0 and ts.cuda_stream == solver.stream()
+        if not same:
+            solver.synchronize()
         exchange_halos(views[0], views[1], views[2], views[3], rank, world, group)
+        if not same:
+            ts.synchronize()
 
+    import torch.distributed as dist
+
+    red_dev = "cpu" if dist.get_backend(group) == "gloo" else f"cuda:{device}"
     solver.set_halo_exchange(exchange)
-    solver.set_dt_reduce(lambda v: min_allreduce(v, device=f"cuda:{device}", group=group))
+    solver.set_dt_reduce(lambda v: min_allreduce(v, device=red_dev, group=group))
     return views
