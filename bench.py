@@ -305,20 +305,34 @@ def main():
                         "source": "profiles/executed_fp64_per_unit.json (ncu executed DFMA/DMUL/DADD per unit) / live CUDA-event time"}
         except Exception:  # noqa: BLE001
             executed = None
-    roof = {
-        "bound": "fp64", "kernel": "face_kernel (3 launches = one face pass per stage)" if dominant == "face"
-        else "cell_kernel (one launch per stage)",
-        "achieved": ach_face if dominant == "face" else ach_cell, "peak": peak, "unit": "TFLOP/s",
-        "frac": (ach_face if dominant == "face" else ach_cell) / peak if peak else None,
-        "traffic": traffic,
-        "peak_source": "live DFMA microbenchmark on this GPU (MEASURED_PEAKS.json has no FP64 entry)",
-        "flops_basis": "algorithmic = reference op count (SURVEY §8a/§8d): 8503 per face point, 162710 per "
-                       "cell-residual; the kernels execute fewer ops (see 'executed'), so frac > 1 means "
-                       "restructured algebra, not more than peak throughput",
-        "executed": executed,
+    # headline: this kernel's own FP64 work (executed DFMA/DMUL/DADD from the
+    # committed ncu capture) per CUDA-event second; the reference's op count
+    # for the same unit (larger: the algebra here is restructured) is kept
+    # beside it as 'reference_op_basis'
+    ref_basis = {
+        "flops_basis": "reference op count (SURVEY §8a/§8d): 8503 per face point, 162710 per cell-residual",
         "face": {"ms_per_stage": face_stage_ms, "tflops": ach_face, "frac": ach_face / peak if peak else None},
         "cell": {"ms_per_stage": cell_stage_ms, "tflops": ach_cell, "frac": ach_cell / peak if peak else None},
         "step_tflops_equiv": F_CELL_STEP.get((a.degree, visc), 0.0) * ncell_glob * a.steps / (el_ms * 1e-3) / 1e12,
+    }
+    if executed is not None:
+        ach = executed["face_tflops"] if dominant == "face" else executed["cell_tflops"]
+        basis = ("executed FP64 flops per unit (2*DFMA + DMUL + DADD, ncu inst counts in "
+                 "profiles/executed_fp64_per_unit.json): %.0f per face point, %.0f per cell-stage"
+                 % (ex["face_point"]["fp64_flops"], ex["cell_stage"]["fp64_flops"]))
+    else:
+        ach = ach_face if dominant == "face" else ach_cell
+        basis = ref_basis["flops_basis"]
+    roof = {
+        "bound": "fp64", "kernel": "face_kernel (3 launches = one face pass per stage)" if dominant == "face"
+        else "cell_kernel (one launch per stage)",
+        "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+        "frac": ach / peak if peak else None,
+        "traffic": traffic,
+        "peak_source": "live DFMA microbenchmark on this GPU (MEASURED_PEAKS.json has no FP64 entry)",
+        "flops_basis": basis,
+        "executed": executed,
+        "reference_op_basis": ref_basis,
     }
 
     cpu = None

@@ -18,8 +18,10 @@ struct Launch {
     using SH = Shape<P, DIM>;
     template <int AXIS = 2>
     static int face_smem() {
-        // double-buffered stage of both neighbours' coefficients
-        return 2 * (2 * SH::NC * 32) * (int)sizeof(double);
+        // staged coefficients of both neighbours (double-buffered by default)
+        // [+ the flux accumulators when they live in shared memory]
+        return (HGKS_FACE_STAGES * (2 * SH::NC * 32) + (HGKS_FACE_ACC_SMEM ? 35 * FaceCTA<P, DIM, AXIS>::NT : 0)) *
+               (int)sizeof(double);
     }
     // persistent face kernels: resident CTAs on the whole GPU per axis
     static inline int face_grid[3] = {0, 0, 0};

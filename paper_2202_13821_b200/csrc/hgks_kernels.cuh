@@ -26,6 +26,14 @@
 #endif
 // P3 face CTAs have 9 warps: one CTA per SM keeps them spill-free
 #define HGKS_FACE_MINB_P(P) ((P) == 3 ? 1 : HGKS_FACE_MINB)
+// face kernel staging buffers (2: double-buffered prefetch, 1: single) and
+// where the 35-double flux accumulator lives (0: registers, 1: shared memory)
+#ifndef HGKS_FACE_STAGES
+#define HGKS_FACE_STAGES 2
+#endif
+#ifndef HGKS_FACE_ACC_SMEM
+#define HGKS_FACE_ACC_SMEM 0
+#endif
 // cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
 #ifndef HGKS_CELL_TC
 #define HGKS_CELL_TC 16
@@ -245,12 +253,15 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_P(P)
     cp_async_commit();
     int n = 0;
     for (int t = t0; t < tile_end; t += step, ++n) {
-        double* sc = smem + (n & 1) * STG;
-        if (t + step < tile_end) prefetch(t + step, smem + ((n + 1) & 1) * STG);
-        cp_async_commit();
+        double* sc = smem + (HGKS_FACE_STAGES == 2 ? (n & 1) * STG : 0);
+        if (HGKS_FACE_STAGES == 2) {
+            if (t + step < tile_end) prefetch(t + step, smem + ((n + 1) & 1) * STG);
+            cp_async_commit();
+        }
         const int i0 = (t % ntx) * 32, j = (t / ntx) % ny, k = t / (ntx * ny);
         const int i = i0 + lane;
-        cp_async_wait<1>();  // this tile's stage
+        if (HGKS_FACE_STAGES == 2) cp_async_wait<1>();  // this tile's stage
+        else cp_async_wait<0>();
         __syncthreads();
 #pragma unroll 1
         for (int ip = 0; ip < PPW; ++ip) {
@@ -264,7 +275,11 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_P(P)
             const double* cL = sc + lane;
             const double* cR = sc + NC * 32 + lane;
 
+#if HGKS_FACE_ACC_SMEM
+            SmemAcc acc{smem + HGKS_FACE_STAGES * STG + tid, NT};
+#else
             FluxAcc acc;
+#endif
             flux_init(acc);
             const bool owned = k < kp.nzl;
             const long item = (long)AXIS * kp.ncells_glob + (long)i + (long)nx * (j + (long)ny * (k + kp.kglob0));
@@ -319,6 +334,10 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_P(P)
         }
         }  // points of this warp
         __syncthreads();  // this stage is free for the prefetch two tiles ahead
+        if (HGKS_FACE_STAGES == 1) {
+            if (t + step < tile_end) prefetch(t + step, smem);
+            cp_async_commit();
+        }
     }
     cp_async_wait<0>();
 }

@@ -278,6 +278,16 @@ struct FluxAcc {
     HD double& nq(int k, int m) { return nq_[k][m]; }
 };
 
+// the same accumulator as a per-thread shared-memory column ([slot][thread]:
+// consecutive lanes hit consecutive 8-byte words)
+struct SmemAcc {
+    double* p;   // &base[tid]
+    int stride;  // threads per CTA
+    HD double& q0(int m) { return p[m * stride]; }
+    HD double& dq0(int d, int m) { return p[(5 + 5 * d + m) * stride]; }
+    HD double& nq(int k, int m) { return p[(20 + 5 * k + m) * stride]; }
+};
+
 template <class Acc>
 HD void flux_init(Acc& acc) {
 #pragma unroll
