@@ -44,7 +44,8 @@ struct hgks_solver {
     bool own_stream = false;
     // device memory
     double *d_tab = nullptr, *d_dx = nullptr, *d_dy = nullptr, *d_dz = nullptr;
-    double *qa = nullptr, *qb = nullptr, *qs = nullptr, *L1 = nullptr, *Lt1 = nullptr;
+    // A = q^n + dt L1 + dt^2/6 Lt1: the only stage-1 residual output stage 2 needs
+    double *qa = nullptr, *qb = nullptr, *qs = nullptr, *A = nullptr;
     double *R = nullptr, *Rt = nullptr, *tmp = nullptr, *tmp2 = nullptr;
     // streamed host step: copy streams and per-chunk events
     cudaStream_t st_up = nullptr, st_dn = nullptr;
@@ -109,6 +110,7 @@ KParams make_params(hgks_solver* s, double dt, int stage) {
     kp.stage = stage;
     kp.count_fluxes = s->count_fluxes ? 1 : 0;
     kp.report = 0;
+    kp.ft_only = 0;
     kp.dt = dt;
     kp.inv_dt = dt != 0.0 ? 1.0 / dt : 0.0;
     kp.two_mu = 2.0 * s->cfg.mu;
@@ -261,11 +263,12 @@ int run_residual(hgks_solver* s, int which, double dt, int stage, int mode, cons
     int rc = fill_ghosts(s, which);
     if (rc) return rc;
     KParams kp = make_params(s, dt, stage);
+    kp.ft_only = mode == MODE_STAGE2;
     ev_record(s, stage * 3 + 0);
     s->ks.face(kp, in, s->face, s->stream, 0, nullptr);
     s->launches += 3;
     ev_record(s, stage * 3 + 1);
-    s->ks.cell(kp, mode, in, s->face, qn, s->L1, s->Lt1, o0, o1, o2, s->stream, 0, nullptr);
+    s->ks.cell(kp, mode, in, s->face, qn, s->A, nullptr, o0, o1, o2, s->stream, 0, nullptr);
     s->launches += 1;
     ev_record(s, stage * 3 + 2);
     CK(cudaGetLastError());
@@ -375,7 +378,7 @@ int hgks_create(const hgks_config* cfg, hgks_solver** out) {
     CK(cudaMemcpy(s->d_dx, dx.data(), dx.size() * sizeof(double), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(s->d_dy, dy.data(), dy.size() * sizeof(double), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(s->d_dz, dz.data(), dz.size() * sizeof(double), cudaMemcpyHostToDevice));
-    for (double** p : {&s->qa, &s->qb, &s->qs, &s->L1, &s->Lt1}) {
+    for (double** p : {&s->qa, &s->qb, &s->qs, &s->A}) {
         CK(cudaMalloc(p, arr));
         CK(cudaMemset(*p, 0, arr));
     }
@@ -395,7 +398,7 @@ int hgks_create(const hgks_config* cfg, hgks_solver** out) {
 
 void hgks_destroy(hgks_solver* s) {
     if (!s) return;
-    for (double* p : {s->d_tab, s->d_dx, s->d_dy, s->d_dz, s->qa, s->qb, s->qs, s->L1, s->Lt1,
+    for (double* p : {s->d_tab, s->d_dx, s->d_dy, s->d_dz, s->qa, s->qb, s->qs, s->A,
                       s->R, s->Rt, s->tmp, s->tmp2, s->face[0], s->face[1], s->face[2], s->d_val, s->d_red,
                       s->d_halo})
         if (p) cudaFree(p);
@@ -475,12 +478,12 @@ int download_faces(hgks_solver* s, int axis, double* host) {
 int step_phase(hgks_solver* s, double dt, int phase) {
     int rc;
     if (phase == 0) {
-        // stage 1: L1, Lt1, q* from q^n (qa)
+        // stage 1: q* and A from q^n (qa)
         rc = reset_error(s);
         if (rc) return rc;
-        return run_residual(s, 0, dt, 0, MODE_STAGE1, nullptr, s->qs, s->L1, s->Lt1);
+        return run_residual(s, 0, dt, 0, MODE_STAGE1, nullptr, s->qs, s->A, nullptr);
     }
-    if (phase == 1)  // stage 2: q^{n+1} into qb from q*, q^n, L1, Lt1
+    if (phase == 1)  // stage 2: q^{n+1} into qb from q* and A
         return run_residual(s, 1, dt, 1, MODE_STAGE2, s->qa, s->qb, nullptr, nullptr);
     const double* inputs[2] = {s->qa, s->qs};
     bool failed = false;
@@ -659,19 +662,21 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
     }
     cudaEventDestroy(start);
     // ---- compute wavefront
-    const KParams kp1 = make_params(s, dt, 0), kp2 = make_params(s, dt, 1);
+    const KParams kp1 = make_params(s, dt, 0);
+    KParams kp2 = make_params(s, dt, 1);
+    kp2.ft_only = 1;
     const KernelSet& K = s->ks;
     cudaStream_t cs = s->stream;
     auto wait_up = [&](int c) { return cudaStreamWaitEvent(cs, s->ev_up[(c + N) % N], 0); };
     auto F1 = [&](int c) { K.face_layers(kp1, s->qa, s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
     auto C1 = [&](int c) {
-        K.cell_layers(kp1, MODE_STAGE1, s->qa, s->face, nullptr, nullptr, nullptr, s->qs, s->L1, s->Lt1, cs,
+        K.cell_layers(kp1, MODE_STAGE1, s->qa, s->face, nullptr, nullptr, nullptr, s->qs, s->A, nullptr, cs,
                       kb(c), kb(c + 1));
         ++s->launches;
     };
     auto F2 = [&](int c) { K.face_layers(kp2, s->qs, s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
     auto C2 = [&](int c) {
-        K.cell_layers(kp2, MODE_STAGE2, s->qs, s->face, s->qa, s->L1, s->Lt1, s->qb, nullptr, nullptr, cs,
+        K.cell_layers(kp2, MODE_STAGE2, s->qs, s->face, nullptr, s->A, nullptr, s->qb, nullptr, nullptr, cs,
                       kb(c), kb(c + 1));
         ++s->launches;
         return cudaEventRecord(s->ev_c2[c], cs);

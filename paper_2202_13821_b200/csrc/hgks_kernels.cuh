@@ -78,6 +78,7 @@ struct KParams {
     int stage;             // 0 first residual of a step, 1 second
     int count_fluxes;
     int report;            // re-run in report mode: write err_val for the winning key
+    int ft_only;           // face pass of S2O4 stage 2: only Ft is consumed, F is not stored
     double dt, inv_dt;
     double two_mu;         // 2 mu: face tau = 2 mu / (p_l + p_r)
     double rh_coef;        // dt / (4 mu): dt / (2 tau) = (p_l + p_r) rh_coef
@@ -324,11 +325,12 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_P(P)
                 Gt[1 + AXIS] = Ft[1];
                 Gt[1 + C1] = Ft[2];
                 Gt[1 + C2] = Ft[3];
+                if (!kp.ft_only) {
 #pragma unroll
-                for (int v = 0; v < 5; ++v) {
-                    out[v * kp.fs] = G[v];
-                    out[(5 + v) * kp.fs] = Gt[v];
+                    for (int v = 0; v < 5; ++v) out[v * kp.fs] = G[v];
                 }
+#pragma unroll
+                for (int v = 0; v < 5; ++v) out[(5 + v) * kp.fs] = Gt[v];
                 if (kp.count_fluxes && owned) atomicAdd(kp.flux_count, 1ull);
             }
         }
@@ -448,32 +450,35 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
             cp_async8(dst + comp * TC + l, qin + comp * kp.cs + cbase + (ok ? i0 + l : 0), ok);
         }
     };
+    // stage 2 consumes only the Ft rows (the face pass stores only those)
+    constexpr int RW = MODE == MODE_STAGE2 ? 5 : 10, RO = 10 - RW;
+    auto face_row = [](int rr) { return (rr / RW) * 10 + RO + rr % RW; };
     auto prefetch_faces = [&](int t) {
         int i0, j, k;
         tile_ijk(t, i0, j, k);
         const long rowk = (long)nx * (j + (long)ny * k);
-        for (int e = tid; e < CT::FX; e += NT) {  // x faces i0 .. i0+TC (periodic wrap at nx)
-            const int l = e % (TC + 1), r = e / (TC + 1);
+        for (int e = tid; e < CT::NFX * RW * (TC + 1); e += NT) {  // x faces i0 .. i0+TC (periodic wrap at nx)
+            const int l = e % (TC + 1), r = face_row(e / (TC + 1));
             const int ig = i0 + l;
             const bool ok = ig <= nx;  // x is always periodic: face nx is face 0
             const int iw = ig == nx ? 0 : ig;
-            cp_async8(fx + e, f0 + (long)r * kp.fs + rowk + (ok ? iw : 0), ok);
+            cp_async8(fx + r * (TC + 1) + l, f0 + (long)r * kp.fs + rowk + (ok ? iw : 0), ok);
         }
         const int jp = j + 1 == ny ? 0 : j + 1;
         const long rowp = (long)nx * (jp + (long)ny * k);
-        for (int e = tid; e < CT::FY; e += NT) {  // y faces of rows j, j+1
-            const int l = e % (2 * TC), r = e / (2 * TC);
+        for (int e = tid; e < CT::NFY * RW * 2 * TC; e += NT) {  // y faces of rows j, j+1
+            const int l = e % (2 * TC), r = face_row(e / (2 * TC));
             const int ig = i0 + (l % TC);
             const bool ok = ig < nx;
-            cp_async8(fy + e, f1 + (long)r * kp.fs + (l < TC ? rowk : rowp) + (ok ? ig : 0), ok);
+            cp_async8(fy + r * 2 * TC + l, f1 + (long)r * kp.fs + (l < TC ? rowk : rowp) + (ok ? ig : 0), ok);
         }
         const int kp1 = (k + 1 == kp.zface_layers && kp.z_wrap) ? 0 : k + 1;
         const long rowz = (long)nx * (j + (long)ny * kp1);
-        for (int e = tid; e < CT::FZ; e += NT) {  // z faces of layers k, k+1
-            const int l = e % (2 * TC), r = e / (2 * TC);
+        for (int e = tid; e < CT::NFZ * RW * 2 * TC; e += NT) {  // z faces of layers k, k+1
+            const int l = e % (2 * TC), r = face_row(e / (2 * TC));
             const int ig = i0 + (l % TC);
             const bool ok = ig < nx;
-            cp_async8(fz + e, f2 + (long)r * kp.fs + (l < TC ? rowk : rowz) + (ok ? ig : 0), ok);
+            cp_async8(fz + r * 2 * TC + l, f2 + (long)r * kp.fs + (l < TC ? rowk : rowz) + (ok ? ig : 0), ok);
         }
     };
 
@@ -601,23 +606,28 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
                     const double L = R[m] * (ctab<P, DIM>.massf[m] * ivol);
                     const long gi = g0 + (long)(m * 5) * kp.cs;
                     if (MODE == MODE_STAGE1) {
-                        (ft ? out2 : out1)[gi] = L;
                         lb[(ft * NC + m * 5 + v) * TC + l] = L;
                     } else {
-                        // q += dt L1 + dt^2/6 (Lt1 + 2 Lt2) (integrator.hpp:72-74)
-                        out0[gi] = __ldg(qn + gi) + (dt * __ldg(L1 + gi) + c6 * (__ldg(Lt1 + gi) + 2.0 * L));
+                        // q^{n+1} = q + dt L1 + dt^2/6 (Lt1 + 2 Lt2) (integrator.hpp:72-74)
+                        // = A + dt^2/6 * 2 Lt2, A formed by stage 1
+                        out0[gi] = __ldg(L1 + gi) + c6 * (2.0 * L);
                     }
                 }
             }
         }
         if (MODE == MODE_STAGE1) {
-            // q* = q + dt/2 L1 + dt^2/8 Lt1 (integrator.hpp:69-70) from shared memory
+            // from shared memory, per coefficient (integrator.hpp:69-74):
+            //   q* = q + dt/2 L1 + dt^2/8 Lt1           -> out0
+            //   A  = q + (dt L1 + dt^2/6 Lt1)           -> out1 (stage 2 adds dt^2/6 * 2 Lt2)
             __syncthreads();
+            const double c6 = dt * dt / 6.0;
             for (int e = tid; e < NC * TC; e += NT) {
                 const int l = e % TC, comp = e / TC;
                 if (i0 + l >= nx) continue;
-                out0[comp * kp.cs + cbase + i0 + l] =
-                    sc[comp * TC + l] + 0.5 * dt * lb[comp * TC + l] + 0.125 * dt * dt * lb[(NC + comp) * TC + l];
+                const double q = sc[comp * TC + l], L = lb[comp * TC + l], Lt = lb[(NC + comp) * TC + l];
+                const long gi = comp * kp.cs + cbase + i0 + l;
+                out0[gi] = q + 0.5 * dt * L + 0.125 * dt * dt * Lt;
+                out1[gi] = q + (dt * L + c6 * Lt);
             }
         }
         __syncthreads();  // buffers of this tile are free for the next prefetch
