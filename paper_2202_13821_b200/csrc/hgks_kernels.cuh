@@ -228,38 +228,54 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_P(P)
     const int tile_end = tile_first + tile_count;
     const int step = kp.report ? tile_count : gridDim.x;
 
-    auto prefetch = [&](int t, double* dst) {
-        const int i0 = (t % ntx) * 32, j = (t / ntx) % ny, k = t / (ntx * ny);
-        for (int e = tid; e < STG; e += NT) {
-            const int l = e & 31;
-            const int row = e >> 5;
-            const int side = row >= NC;
-            const int comp = row - side * NC;
-            const int i = i0 + l;
-            const bool ok = i < nx;
-            int ci = ok ? i : 0, cj = j, ck = k;
-            if (!side) {
-                if (AXIS == 0) ci = (ci == 0 ? nx - 1 : ci - 1);
-                if (AXIS == 1) cj = (j == 0 ? ny - 1 : j - 1);
-                if (AXIS == 2) ck = k - 1;
-            }
-            cp_async8(dst + e, q + comp * kp.cs + (long)(ck + 1) * kp.S + (long)cj * nx + ci, ok);
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    // tile t -> (x offset, row j, layer k); computed once per tile
+    struct TI {
+        int i0, j, k;
+    };
+    auto tile_of = [&](int t) {
+        const int a = t / ntx;
+        TI r;
+        r.i0 = (t - a * ntx) * 32;
+        r.k = a / ny;
+        r.j = a - r.k * ny;
+        return r;
+    };
+    // both neighbours' coefficients of one tile: lane = face, rows = components
+    // (each warp streams its share of the 2*NC rows, 256 B per row)
+    auto prefetch = [&](const TI& ti, double* dst) {
+        const int i = ti.i0 + lane;
+        const bool ok = i < nx;
+        const int ci = ok ? i : 0;
+        int mi = ci, mj = ti.j, mk = ti.k;
+        if (AXIS == 0) mi = ci == 0 ? nx - 1 : ci - 1;
+        if (AXIS == 1) mj = ti.j == 0 ? ny - 1 : ti.j - 1;
+        if (AXIS == 2) mk = ti.k - 1;
+        const double* sL = q + (long)(mk + 1) * kp.S + (long)mj * nx + mi;
+        const double* sR = q + (long)(ti.k + 1) * kp.S + (long)ti.j * nx + ci;
+        constexpr int NW = NT / 32;
+#pragma unroll 4
+        for (int c = warp; c < NC; c += NW) {
+            cp_async8(dst + c * 32 + lane, sL + c * kp.cs, ok);
+            cp_async8(dst + (NC + c) * 32 + lane, sR + c * kp.cs, ok);
         }
     };
 
-    const int lane = tid & 31;
-    const int warp = tid >> 5;
     const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
-    if (t0 < tile_end) prefetch(t0, smem);
+    TI cur = tile_of(t0);
+    if (t0 < tile_end) prefetch(cur, smem);
     cp_async_commit();
     int n = 0;
     for (int t = t0; t < tile_end; t += step, ++n) {
         double* sc = smem + (HGKS_FACE_STAGES == 2 ? (n & 1) * STG : 0);
+        const bool has_next = t + step < tile_end;
+        const TI nxt = has_next ? tile_of(t + step) : cur;
         if (HGKS_FACE_STAGES == 2) {
-            if (t + step < tile_end) prefetch(t + step, smem + ((n + 1) & 1) * STG);
+            if (has_next) prefetch(nxt, smem + ((n + 1) & 1) * STG);
             cp_async_commit();
         }
-        const int i0 = (t % ntx) * 32, j = (t / ntx) % ny, k = t / (ntx * ny);
+        const int i0 = cur.i0, j = cur.j, k = cur.k;
         const int i = i0 + lane;
         if (HGKS_FACE_STAGES == 2) cp_async_wait<1>();  // this tile's stage
         else cp_async_wait<0>();
@@ -337,9 +353,10 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_P(P)
         }  // points of this warp
         __syncthreads();  // this stage is free for the prefetch two tiles ahead
         if (HGKS_FACE_STAGES == 1) {
-            if (t + step < tile_end) prefetch(t + step, smem);
+            if (has_next) prefetch(nxt, smem);
             cp_async_commit();
         }
+        cur = nxt;
     }
     cp_async_wait<0>();
 }
@@ -435,27 +452,30 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
     const int tile_end = tile_first + tile_count;
     const int step = kp.report ? tile_count : gridDim.x;
 
-    auto tile_ijk = [&](int t, int& i0, int& j, int& k) {
-        i0 = (t % ntx) * TC;
-        j = (t / ntx) % ny;
-        k = t / (ntx * ny);
-    };
-    auto prefetch_coef = [&](int t, double* dst) {
+    struct TI {
         int i0, j, k;
-        tile_ijk(t, i0, j, k);
-        const long cbase = (long)(k + 1) * kp.S + (long)j * nx;
+    };
+    auto tile_of = [&](int t) {
+        const int a = t / ntx;
+        TI r;
+        r.i0 = (t - a * ntx) * TC;
+        r.k = a / ny;
+        r.j = a - r.k * ny;
+        return r;
+    };
+    auto prefetch_coef = [&](const TI& ti, double* dst) {
+        const long cbase = (long)(ti.k + 1) * kp.S + (long)ti.j * nx;
         for (int e = tid; e < CT::COEF; e += NT) {
             const int l = e % TC, comp = e / TC;
-            const bool ok = i0 + l < nx;
-            cp_async8(dst + comp * TC + l, qin + comp * kp.cs + cbase + (ok ? i0 + l : 0), ok);
+            const bool ok = ti.i0 + l < nx;
+            cp_async8(dst + comp * TC + l, qin + comp * kp.cs + cbase + (ok ? ti.i0 + l : 0), ok);
         }
     };
     // stage 2 consumes only the Ft rows (the face pass stores only those)
     constexpr int RW = MODE == MODE_STAGE2 ? 5 : 10, RO = 10 - RW;
     auto face_row = [](int rr) { return (rr / RW) * 10 + RO + rr % RW; };
-    auto prefetch_faces = [&](int t) {
-        int i0, j, k;
-        tile_ijk(t, i0, j, k);
+    auto prefetch_faces = [&](const TI& ti) {
+        const int i0 = ti.i0, j = ti.j, k = ti.k;
         const long rowk = (long)nx * (j + (long)ny * k);
         for (int e = tid; e < CT::NFX * RW * (TC + 1); e += NT) {  // x faces i0 .. i0+TC (periodic wrap at nx)
             const int l = e % (TC + 1), r = face_row(e / (TC + 1));
@@ -483,18 +503,20 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
     };
 
     const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
-    if (t0 < tile_end) prefetch_coef(t0, coefb);
+    TI cur = tile_of(t0);
+    if (t0 < tile_end) prefetch_coef(cur, coefb);
     cp_async_commit();
     const double dt = kp.dt;
     int n = 0;
     for (int t = t0; t < tile_end; t += step, ++n) {
         double* sc = coefb + (n & 1) * CT::COEF;
-        prefetch_faces(t);
+        prefetch_faces(cur);
         cp_async_commit();
-        if (t + step < tile_end) prefetch_coef(t + step, coefb + ((n + 1) & 1) * CT::COEF);
+        const bool has_next = t + step < tile_end;
+        const TI nxt = has_next ? tile_of(t + step) : cur;
+        if (has_next) prefetch_coef(nxt, coefb + ((n + 1) & 1) * CT::COEF);
         cp_async_commit();
-        int i0, j, k;
-        tile_ijk(t, i0, j, k);
+        const int i0 = cur.i0, j = cur.j, k = cur.k;
         const long cbase = (long)(k + 1) * kp.S + (long)j * nx;
         const double hy = __ldg(kp.dy + j), hz = __ldg(kp.dz + k + 1);
         const double i2hy = __ldg(kp.i2dy + j), i2hz = __ldg(kp.i2dz + k + 1);
@@ -631,6 +653,7 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
             }
         }
         __syncthreads();  // buffers of this tile are free for the next prefetch
+        cur = nxt;
     }
     cp_async_wait<0>();
 }
