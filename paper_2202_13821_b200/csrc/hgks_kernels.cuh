@@ -182,6 +182,109 @@ __device__ __forceinline__ void face_trace_rt(int p, int side, const double* c, 
     }
 }
 
+// ---- sign symmetry of the 2-point Gauss rule (P1/P2)
+// The rule's abscissae are +-g on every axis and P_l(-x) = (-1)^l P_l(x)
+// exactly in floating point, so a table row at point p equals the row at the
+// all-positive point with basis n negated by prod_a s_a^{par_a(n)} (a
+// derivative along axis a carries one more s_a). Flipping the sign bit of
+// the coefficient (an integer op) instead of instantiating one evaluator per
+// point gives a single code path for every point and bitwise the same
+// products and sums; the symmetry of the tables is checked at compile time.
+constexpr unsigned kSignBit = 0x80000000u;
+__device__ __forceinline__ double flip_sign(double x, unsigned m) {
+    return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
+}
+
+template <int P, int DIM>
+constexpr bool gauss2_symmetric() {
+    constexpr ct::Tab T = ct::make_tab<P, DIM>();
+    const int nqz = DIM == 3 ? 2 : 1;
+    auto sg = [](bool neg, int par) { return (neg && par) ? -1.0 : 1.0; };
+    // volume points p = (i*2 + j)*nqz + k; canonical p* = NVP - 1
+    for (int p = 0; p < T.NVP; ++p) {
+        const bool ni = p / (2 * nqz) == 0, nj = (p / nqz) % 2 == 0, nk = nqz == 2 && p % nqz == 0;
+        for (int n = 0; n < T.N; ++n) {
+            const double sn = sg(ni, T.par[0][n]) * sg(nj, T.par[1][n]) * sg(nk, T.par[2][n]);
+            if (T.vB[p][n] != sn * T.vB[T.NVP - 1][n]) return false;
+            const double sa[3] = {ni ? -1.0 : 1.0, nj ? -1.0 : 1.0, nk ? -1.0 : 1.0};
+            for (int a = 0; a < 3; ++a)
+                if (T.vdB[p][a][n] != sa[a] * sn * T.vdB[T.NVP - 1][a][n]) return false;
+        }
+    }
+    // face points p = ib * nc + ic over the tangential axes (C1, C2)
+    for (int a = 0; a < 3; ++a) {
+        const int c1 = (a + 1) % 3, c2 = (a + 2) % 3;
+        const int nb = (c1 == 2 && DIM == 2) ? 1 : 2, nc = (c2 == 2 && DIM == 2) ? 1 : 2;
+        const int ps = (nb - 1) * nc + (nc - 1);
+        for (int sd = 0; sd < 2; ++sd)
+            for (int p = 0; p < nb * nc; ++p) {
+                const bool n1 = nb == 2 && p / nc == 0, n2 = nc == 2 && p % nc == 0;
+                for (int n = 0; n < T.N; ++n) {
+                    const double sn = sg(n1, T.par[c1][n]) * sg(n2, T.par[c2][n]);
+                    if (T.fB[a][sd][p][n] != sn * T.fB[a][sd][ps][n]) return false;
+                    for (int d = 0; d < 3; ++d) {
+                        const double sd1 = d == c1 && n1 ? -1.0 : 1.0, sd2 = d == c2 && n2 ? -1.0 : 1.0;
+                        if (T.fdB[a][sd][p][d][n] != sd1 * sd2 * sn * T.fdB[a][sd][ps][d][n]) return false;
+                    }
+                }
+            }
+    }
+    return true;
+}
+
+// face_trace for the 2-point rule: one code path for all face points
+template <int P, int DIM, int AXIS, int SIDE>
+__device__ __forceinline__ void face_trace_sym(int p, const double* __restrict__ c, const double* i2h,
+                                               double* t) {
+    using SH = Shape<P, DIM>;
+    static_assert(SH::NQ == 2, "sign-symmetric traces need the 2-point rule");
+    static_assert(gauss2_symmetric<P, DIM>(), "basis tables are not sign-symmetric");
+    constexpr int N = SH::N;
+    constexpr int C1 = (AXIS + 1) % 3, C2 = (AXIS + 2) % 3;
+    constexpr int NB = (C1 == 2 && DIM == 2) ? 1 : 2, NCC = (C2 == 2 && DIM == 2) ? 1 : 2;
+    constexpr int PS = (NB - 1) * NCC + (NCC - 1);
+    constexpr int SI = SIDE == 0 ? 1 : 0;
+    const unsigned m1 = (NB == 2 && p / NCC == 0) ? kSignBit : 0u;
+    const unsigned m2 = (NCC == 2 && p % NCC == 0) ? kSignBit : 0u;
+    double e[20];
+#pragma unroll
+    for (int m = 0; m < 20; ++m) e[m] = 0.0;
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+        const double b = ctab<P, DIM>.fB[AXIS][SI][PS][n];
+        const double d0 = ctab<P, DIM>.fdB[AXIS][SI][PS][0][n];
+        const double d1 = ctab<P, DIM>.fdB[AXIS][SI][PS][1][n];
+        const double d2 = ctab<P, DIM>.fdB[AXIS][SI][PS][2][n];
+        const unsigned mn = (ctab<P, DIM>.par[C1][n] ? m1 : 0u) ^ (ctab<P, DIM>.par[C2][n] ? m2 : 0u);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+            const double cv = flip_sign(c[(n * 5 + v) * 32], mn);
+            if (b != 0.0) e[v] += b * cv;
+            if (d0 != 0.0) e[5 + v] += d0 * cv;
+            if (d1 != 0.0) e[10 + v] += d1 * cv;
+            if (d2 != 0.0) e[15 + v] += d2 * cv;
+        }
+    }
+    constexpr int g[3] = {AXIS, C1, C2};
+    t[0] = e[0];
+    t[1] = e[1 + AXIS];
+    t[2] = e[1 + C1];
+    t[3] = e[1 + C2];
+    t[4] = e[4];
+#pragma unroll
+    for (int d = 1; d < 4; ++d) {
+        const int gd = g[d - 1];
+        const double* src = e + 5 + 5 * gd;
+        // derivative along a tangential axis carries that axis' point sign
+        const double sf = flip_sign(i2h[gd], gd == C1 ? m1 : gd == C2 ? m2 : 0u);
+        t[5 * d + 0] = sf * src[0];
+        t[5 * d + 1] = sf * src[1 + AXIS];
+        t[5 * d + 2] = sf * src[1 + C1];
+        t[5 * d + 3] = sf * src[1 + C2];
+        t[5 * d + 4] = sf * src[4];
+    }
+}
+
 // async global->shared copies (cp.async, LDGSTS): the persistent kernels
 // prefetch the next tile while computing the current one
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
@@ -305,7 +408,12 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_P(P)
 #pragma unroll 1
             for (int side = 0; side < 2 && !fail; ++side) {
                 double tr[20];
-                face_trace_rt<P, DIM, AXIS, NFP>(p, side, side == 0 ? cL : cR, side == 0 ? i2hL : i2hR, tr);
+                if constexpr (SH::NQ == 2) {
+                    if (side == 0) face_trace_sym<P, DIM, AXIS, 0>(p, cL, i2hL, tr);
+                    else face_trace_sym<P, DIM, AXIS, 1>(p, cR, i2hR, tr);
+                } else {
+                    face_trace_rt<P, DIM, AXIS, NFP>(p, side, side == 0 ? cL : cR, side == 0 ? i2hL : i2hR, tr);
+                }
                 double bad = 0.0, ps = 0.0;
                 const int rc = flux_side<VISC>(tr, side, kp.gas, acc, ps, bad);
                 psum += ps;
@@ -392,6 +500,48 @@ __device__ __forceinline__ void vol_eval(const double* __restrict__ c, const dou
         e[5 + v] *= i2h[0];
         e[10 + v] *= i2h[1];
         e[15 + v] *= i2h[2];
+    }
+}
+
+// vol_eval for the 2-point rule: one code path for all volume points
+// (sign symmetry, see face_trace_sym)
+template <int P, int DIM, int TC>
+__device__ __forceinline__ void vol_eval_sym(int p, const double* __restrict__ c, const double* i2h,
+                                             double* e) {
+    using SH = Shape<P, DIM>;
+    static_assert(SH::NQ == 2, "sign-symmetric evaluation needs the 2-point rule");
+    static_assert(gauss2_symmetric<P, DIM>(), "basis tables are not sign-symmetric");
+    constexpr int N = SH::N, NVP = SH::NVP;
+    constexpr int NQZ = DIM == 3 ? 2 : 1;
+    constexpr int PS = NVP - 1;
+    const unsigned m0 = p / (2 * NQZ) == 0 ? kSignBit : 0u;
+    const unsigned m1 = (p / NQZ) % 2 == 0 ? kSignBit : 0u;
+    const unsigned m2 = (NQZ == 2 && p % NQZ == 0) ? kSignBit : 0u;
+#pragma unroll
+    for (int m = 0; m < 20; ++m) e[m] = 0.0;
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+        const double b = ctab<P, DIM>.vB[PS][n];
+        const double d0 = ctab<P, DIM>.vdB[PS][0][n];
+        const double d1 = ctab<P, DIM>.vdB[PS][1][n];
+        const double d2 = ctab<P, DIM>.vdB[PS][2][n];
+        const unsigned mn = (ctab<P, DIM>.par[0][n] ? m0 : 0u) ^ (ctab<P, DIM>.par[1][n] ? m1 : 0u) ^
+                            (ctab<P, DIM>.par[2][n] ? m2 : 0u);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+            const double cv = flip_sign(c[(n * 5 + v) * TC], mn);
+            if (b != 0.0) e[v] += b * cv;
+            if (d0 != 0.0) e[5 + v] += d0 * cv;
+            if (d1 != 0.0) e[10 + v] += d1 * cv;
+            if (d2 != 0.0) e[15 + v] += d2 * cv;
+        }
+    }
+    const double s0 = flip_sign(i2h[0], m0), s1 = flip_sign(i2h[1], m1), s2 = flip_sign(i2h[2], m2);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+        e[5 + v] *= s0;
+        e[10 + v] *= s1;
+        e[15 + v] *= s2;
     }
 }
 
@@ -531,7 +681,8 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
             if (i >= nx) continue;
             const double i2h[3] = {__ldg(kp.i2dx + i), i2hy, i2hz};
             double e[20];
-            vol_eval_rt<P, DIM, TC, NVP>(p, sc + l, i2h, e);
+            if constexpr (SH::NQ == 2) vol_eval_sym<P, DIM, TC>(p, sc + l, i2h, e);
+            else vol_eval_rt<P, DIM, TC, NVP>(p, sc + l, i2h, e);
             double o[30];
             double bad = 0.0;
             const int rc = smooth_flux<VISC, NAX>(e, kp.gas, o, bad);
