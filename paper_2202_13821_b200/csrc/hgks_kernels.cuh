@@ -34,6 +34,11 @@
 #ifndef HGKS_FACE_ACC_SMEM
 #define HGKS_FACE_ACC_SMEM 0
 #endif
+// threads of the 3-D P1/P2 cell kernel (0: one per (cell, volume point));
+// 160 = one per (cell, var, F|Ft) item of the stage-1 projection, 10 warps/SM
+#ifndef HGKS_CELL_NT3
+#define HGKS_CELL_NT3 160
+#endif
 // cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
 #ifndef HGKS_CELL_TC
 #define HGKS_CELL_TC 16
@@ -62,7 +67,7 @@ struct Shape {
     // cell tile along x and threads of the cell kernel (one thread per
     // (cell, volume point) in phase B for P1/P2)
     static constexpr int TC = P == 3 ? 8 : HGKS_CELL_TC;
-    static constexpr int NT_CELL = P == 3 ? 224 : HGKS_CELL_TC * NVP;
+    static constexpr int NT_CELL = P == 3 ? 224 : (DIM == 3 && HGKS_CELL_NT3 > 0) ? HGKS_CELL_NT3 : HGKS_CELL_TC * NVP;
     static constexpr int MINB_CELL = P == 3 ? 1 : (HGKS_CELL_TC <= 16 ? 2 : 1);
 };
 
@@ -627,35 +632,80 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
     auto prefetch_faces = [&](const TI& ti) {
         const int i0 = ti.i0, j = ti.j, k = ti.k;
         const long rowk = (long)nx * (j + (long)ny * k);
-        for (int e = tid; e < CT::NFX * RW * (TC + 1); e += NT) {  // x faces i0 .. i0+TC (periodic wrap at nx)
-            const int l = e % (TC + 1), r = face_row(e / (TC + 1));
-            const int ig = i0 + l;
-            const bool ok = ig <= nx;  // x is always periodic: face nx is face 0
-            const int iw = ig == nx ? 0 : ig;
-            cp_async8(fx + r * (TC + 1) + l, f0 + (long)r * kp.fs + rowk + (ok ? iw : 0), ok);
-        }
         const int jp = j + 1 == ny ? 0 : j + 1;
         const long rowp = (long)nx * (jp + (long)ny * k);
-        for (int e = tid; e < CT::NFY * RW * 2 * TC; e += NT) {  // y faces of rows j, j+1
-            const int l = e % (2 * TC), r = face_row(e / (2 * TC));
-            const int ig = i0 + (l % TC);
-            const bool ok = ig < nx;
-            cp_async8(fy + r * 2 * TC + l, f1 + (long)r * kp.fs + (l < TC ? rowk : rowp) + (ok ? ig : 0), ok);
-        }
         const int kp1 = (k + 1 == kp.zface_layers && kp.z_wrap) ? 0 : k + 1;
         const long rowz = (long)nx * (j + (long)ny * kp1);
-        for (int e = tid; e < CT::NFZ * RW * 2 * TC; e += NT) {  // z faces of layers k, k+1
-            const int l = e % (2 * TC), r = face_row(e / (2 * TC));
-            const int ig = i0 + (l % TC);
+        if constexpr (2 * TC == 32) {
+            // one face row per warp instruction: x rows hold TC+1 faces
+            // (lanes 0..TC), y/z rows the TC faces of both neighbour rows
+            constexpr int NW = NT / 32;
+            const int lane = tid & 31, warp = tid >> 5;
+            const int igx = i0 + lane;
+            const bool okx = lane <= TC && igx <= nx;  // x is periodic: face nx is face 0
+            const long ox = rowk + (okx ? (igx == nx ? 0 : igx) : 0);
+            const int ig = i0 + (lane % TC);
             const bool ok = ig < nx;
-            cp_async8(fz + r * 2 * TC + l, f2 + (long)r * kp.fs + (l < TC ? rowk : rowz) + (ok ? ig : 0), ok);
+            const long oy = (lane < TC ? rowk : rowp) + (ok ? ig : 0);
+            const long oz = (lane < TC ? rowk : rowz) + (ok ? ig : 0);
+            for (int rr = warp; rr < CT::NFX * RW; rr += NW) {
+                const int r = face_row(rr);
+                if (lane <= TC) cp_async8(fx + r * (TC + 1) + lane, f0 + (long)r * kp.fs + ox, okx);
+            }
+            for (int rr = warp; rr < CT::NFY * RW; rr += NW) {
+                const int r = face_row(rr);
+                cp_async8(fy + r * 2 * TC + lane, f1 + (long)r * kp.fs + oy, ok);
+            }
+            for (int rr = warp; rr < CT::NFZ * RW; rr += NW) {
+                const int r = face_row(rr);
+                cp_async8(fz + r * 2 * TC + lane, f2 + (long)r * kp.fs + oz, ok);
+            }
+        } else {
+            for (int e = tid; e < CT::NFX * RW * (TC + 1); e += NT) {  // x faces i0 .. i0+TC (periodic wrap at nx)
+                const int l = e % (TC + 1), r = face_row(e / (TC + 1));
+                const int ig = i0 + l;
+                const bool ok = ig <= nx;  // x is always periodic: face nx is face 0
+                const int iw = ig == nx ? 0 : ig;
+                cp_async8(fx + r * (TC + 1) + l, f0 + (long)r * kp.fs + rowk + (ok ? iw : 0), ok);
+            }
+            for (int e = tid; e < CT::NFY * RW * 2 * TC; e += NT) {  // y faces of rows j, j+1
+                const int l = e % (2 * TC), r = face_row(e / (2 * TC));
+                const int ig = i0 + (l % TC);
+                const bool ok = ig < nx;
+                cp_async8(fy + r * 2 * TC + l, f1 + (long)r * kp.fs + (l < TC ? rowk : rowp) + (ok ? ig : 0), ok);
+            }
+            for (int e = tid; e < CT::NFZ * RW * 2 * TC; e += NT) {  // z faces of layers k, k+1
+                const int l = e % (2 * TC), r = face_row(e / (2 * TC));
+                const int ig = i0 + (l % TC);
+                const bool ok = ig < nx;
+                cp_async8(fz + r * 2 * TC + l, f2 + (long)r * kp.fs + (l < TC ? rowk : rowz) + (ok ? ig : 0), ok);
+            }
         }
+    };
+    // every item of this thread is cell lt of the tile (NT % TC == 0), so its
+    // widths are loaded one tile ahead into registers
+    static_assert(NT % TC == 0, "cell items must keep their column");
+    const int lt = tid % TC;
+    struct Geo {
+        double hx, i2hx, hy, hz, i2hy, i2hz;
+    };
+    auto geo_of = [&](const TI& ti) {
+        const int i = ti.i0 + lt < nx ? ti.i0 + lt : 0;
+        Geo g;
+        g.hx = __ldg(kp.dx + i);
+        g.i2hx = __ldg(kp.i2dx + i);
+        g.hy = __ldg(kp.dy + ti.j);
+        g.hz = __ldg(kp.dz + ti.k + 1);
+        g.i2hy = __ldg(kp.i2dy + ti.j);
+        g.i2hz = __ldg(kp.i2dz + ti.k + 1);
+        return g;
     };
 
     const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
     TI cur = tile_of(t0);
     if (t0 < tile_end) prefetch_coef(cur, coefb);
     cp_async_commit();
+    Geo gcur = t0 < tile_end ? geo_of(cur) : Geo{};
     const double dt = kp.dt;
     int n = 0;
     for (int t = t0; t < tile_end; t += step, ++n) {
@@ -666,10 +716,11 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
         const TI nxt = has_next ? tile_of(t + step) : cur;
         if (has_next) prefetch_coef(nxt, coefb + ((n + 1) & 1) * CT::COEF);
         cp_async_commit();
+        const Geo gnxt = geo_of(nxt);
         const int i0 = cur.i0, j = cur.j, k = cur.k;
         const long cbase = (long)(k + 1) * kp.S + (long)j * nx;
-        const double hy = __ldg(kp.dy + j), hz = __ldg(kp.dz + k + 1);
-        const double i2hy = __ldg(kp.i2dy + j), i2hz = __ldg(kp.i2dz + k + 1);
+        const double hy = gcur.hy, hz = gcur.hz;
+        const double i2hy = gcur.i2hy, i2hz = gcur.i2hz;
         const long cglob_row = (long)nx * (j + (long)ny * (k + kp.kglob0));
         cp_async_wait<2>();  // this tile's coefficients
         __syncthreads();
@@ -679,7 +730,7 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
             const int l = it % TC, p = it / TC;
             const int i = i0 + l;
             if (i >= nx) continue;
-            const double i2h[3] = {__ldg(kp.i2dx + i), i2hy, i2hz};
+            const double i2h[3] = {gcur.i2hx, i2hy, i2hz};
             double e[20];
             if constexpr (SH::NQ == 2) vol_eval_sym<P, DIM, TC>(p, sc + l, i2h, e);
             else vol_eval_rt<P, DIM, TC, NVP>(p, sc + l, i2h, e);
@@ -706,8 +757,8 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
             const int v = vv % 5, ft = FT0 + vv / 5;  // ft: 0 -> F (R), 1 -> Ft (Rt)
             const int i = i0 + l;
             if (i >= nx) continue;
-            const double hx = __ldg(kp.dx + i);
-            const double i2h[3] = {__ldg(kp.i2dx + i), i2hy, i2hz};
+            const double hx = gcur.hx;
+            const double i2h[3] = {gcur.i2hx, i2hy, i2hz};
             const int row = 5 * ft + v;
             double R[N];
 #pragma unroll
@@ -805,6 +856,7 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
         }
         __syncthreads();  // buffers of this tile are free for the next prefetch
         cur = nxt;
+        gcur = gnxt;
     }
     cp_async_wait<0>();
 }
