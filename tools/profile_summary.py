@@ -38,6 +38,29 @@ def to_bytes(v, unit):
     return num(v) * f
 
 
+def fp64_per_launch(rep):
+    """Executed DFMA / DMUL / DADD thread instructions of the captured launch,
+    summed over the source page's SASS rows."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+    h = rows[hi]
+    si, ti = h.index("Source"), h.index("Thread Instructions Executed")
+    tot = {"dfma": 0.0, "dmul": 0.0, "dadd": 0.0}
+    for r in rows[hi + 1:]:
+        if len(r) != len(h):
+            continue
+        op = r[si].split()
+        if not op:
+            continue
+        o = op[1] if op[0].startswith("@") and len(op) > 1 else op[0]
+        for k in tot:
+            if o.startswith(k.upper()):
+                tot[k] += num(r[ti])
+    return tot
+
+
 def main(tag):
     os.makedirs(PROF, exist_ok=True)
     md = [f"# ncu summary {tag}", ""]
@@ -98,6 +121,25 @@ def main(tag):
         md.append("")
         traffic[name] = {"dram_bytes_per_launch": rd + wr, "read": rd, "write": wr, "duration_ms": dur_ms,
                          "kernel": v.get("Kernel Name", "")}
+    # executed FP64 work per unit (bench.py's roofline basis): face launch = one
+    # axis pass over ncells * NFP points; cell launch = one stage over ncells
+    if bench and all(os.path.exists(os.path.join(OUT, f"prof_{n}.ncu-rep")) for n in ("face", "cell")):
+        ncells = bench["config"]["cells"]
+        nfp = {1: 4, 2: 4, 3: 9}[bench["config"]["degree"]]
+        ex = {}
+        for name, units in (("face_point", ncells * nfp), ("cell_stage", ncells)):
+            t = fp64_per_launch(os.path.join(OUT, f"prof_{name.split('_')[0]}.ncu-rep"))
+            ex[name] = {k: v / units for k, v in t.items()}
+            ex[name]["fp64_flops"] = 2 * ex[name]["dfma"] + ex[name]["dmul"] + ex[name]["dadd"]
+            ex[name]["kernel"] = traffic[name.split("_")[0]]["kernel"][:60]
+        ex["source"] = f"ncu --set full source page, {tag}; units: face = cells*NFP points per launch, cell = cells"
+        json.dump(ex, open(os.path.join(PROF, "executed_fp64_per_unit.json"), "w"), indent=1)
+        md += ["## executed FP64 per unit", "",
+               f"- face point: {ex['face_point']['dfma']:.0f} DFMA + {ex['face_point']['dmul']:.0f} DMUL + "
+               f"{ex['face_point']['dadd']:.0f} DADD = {ex['face_point']['fp64_flops']:.0f} flops "
+               f"(reference op count 8,503)",
+               f"- cell stage: {ex['cell_stage']['dfma']:.0f} DFMA + {ex['cell_stage']['dmul']:.0f} DMUL + "
+               f"{ex['cell_stage']['dadd']:.0f} DADD = {ex['cell_stage']['fp64_flops']:.0f} flops", ""]
     open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
     if "face" in traffic:
         t = traffic["face"]
