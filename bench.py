@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--cfl", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=32, help="z-chunks of the streamed host-vector step")
     ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of CPU reference work")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo = host-staged halo exchange (multi-rank test mode on one GPU)")
@@ -248,7 +249,7 @@ def main():
         q_pin = torch.empty(s.ncoeffs, dtype=torch.float64, pin_memory=True)
         q = q_pin.numpy()
         q[:], _ = s.get_state()
-        nch = 16 if world == 1 else 1  # the streamed step pipelines a single slab
+        nch = a.e2e_chunks if world == 1 else 1  # the streamed step pipelines a single slab
         for _ in range(2):
             s.two_stage_step_host_streamed(q, s.compute_dt(cfl), nch)
         if world > 1:

@@ -26,6 +26,8 @@
 #endif
 // P3 face CTAs have 9 warps: one CTA per SM keeps them spill-free
 #define HGKS_FACE_MINB_P(P) ((P) == 3 ? 1 : HGKS_FACE_MINB)
+// the inviscid flux fits 3 CTAs/SM without spills (166 registers)
+#define HGKS_FACE_MINB_PV(P, VISC) ((P) == 3 ? 1 : (VISC) ? HGKS_FACE_MINB : 3)
 // face kernel staging buffers (2: double-buffered prefetch, 1: single) and
 // where the 35-double flux accumulator lives (0: registers, 1: shared memory)
 #ifndef HGKS_FACE_STAGES
@@ -318,7 +320,7 @@ struct FaceCTA {
 };
 
 template <int P, int DIM, bool VISC, int AXIS>
-__global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_P(P))
+__global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P, VISC))
     face_kernel(KParams kp, const double* __restrict__ q, double* __restrict__ face,
                 int tile_first, int tile_count, int unused) {
     using SH = Shape<P, DIM>;
@@ -400,8 +402,12 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_P(P)
             const double* cL = sc + lane;
             const double* cR = sc + NC * 32 + lane;
 
-#if HGKS_FACE_ACC_SMEM
+#if HGKS_FACE_ACC_SMEM == 1
             SmemAcc acc{smem + HGKS_FACE_STAGES * STG + tid, NT};
+#elif HGKS_FACE_ACC_SMEM == 2
+            HybridAcc acc;
+            acc.p = smem + HGKS_FACE_STAGES * STG + tid;
+            acc.stride = NT;
 #else
             FluxAcc acc;
 #endif

@@ -328,6 +328,19 @@ struct SmemAcc {
     HD double& nq(int k, int m) { return p[(20 + 5 * k + m) * stride]; }
 };
 
+// q0 and dq0 in registers, the non-equilibrium moments (touched once per side
+// and once in the merge) in a per-thread shared-memory column: 30 fewer
+// live registers through the side passes
+struct HybridAcc {
+    double q0_[5];
+    double dq0_[3][5];
+    double* p;   // &base[tid]
+    int stride;  // threads per CTA
+    HD double& q0(int m) { return q0_[m]; }
+    HD double& dq0(int d, int m) { return dq0_[d][m]; }
+    HD double& nq(int k, int m) { return p[(5 * k + m) * stride]; }
+};
+
 template <class Acc>
 HD void flux_init(Acc& acc) {
 #pragma unroll
@@ -363,9 +376,11 @@ HD int flux_side(const double* t, int side, const GasC& g, Acc& acc, double& p_s
     if (rc) return rc;
     p_side = w.rho * w.il;
     const SolveC sc = solve_consts(w, g);
-    Tab<6, 5> tb;  // U: half table (orders 0..6); V, W full
+    // One table object: V, W full; U first full (for A), then overwritten by
+    // this side's half table, so the two U sequences are never live together
+    // (the side pass peaks below 168 registers less often).
+    Tab<6, 5> tb;
     const double il = w.il;
-    half_seq<6>(w.U, w.lam, il, side == 0 ? +1 : -1, tb.U);
     full_seq<5>(w.V, il, tb.V);
     full_seq<5>(w.W, il, tb.W);
     tb.xi2 = g.K * il;
@@ -373,6 +388,13 @@ HD int flux_side(const double* t, int side, const GasC& g, Acc& acc, double& p_s
     Slope a[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) a[d] = micro_slope(sc, w.inv_rho, t + 5 + 5 * d);
+    Slope A{};
+    if (VISCOUS) {
+        // A from compatibility with the full table (flux.hpp:109-110)
+        full_seq<5>(w.U, il, tb.U);
+        A = time_coefficient(sc, tb, a);
+    }
+    half_seq<6>(w.U, w.lam, il, side == 0 ? +1 : -1, tb.U);
     double r[5];
     psi_moment<0, 0, 0>(tb.U, tb, r);
 #pragma unroll
@@ -384,17 +406,6 @@ HD int flux_side(const double* t, int side, const GasC& g, Acc& acc, double& p_s
         for (int m = 0; m < 5; ++m) acc.dq0(d, m) += w.rho * r[m];
     }
     if (VISCOUS) {
-        // A from compatibility with the full table (flux.hpp:109-110)
-        Tab<5, 5> tf;
-        full_seq<5>(w.U, il, tf.U);
-#pragma unroll
-        for (int n = 0; n <= 5; ++n) {
-            tf.V[n] = tb.V[n];
-            tf.W[n] = tb.W[n];
-        }
-        tf.xi2 = tb.xi2;
-        tf.dxi = tb.dxi;
-        const Slope A = time_coefficient(sc, tf, a);
         // free-streaming moments of this side (flux.hpp:112-121), unweighted
         psi_moment<1, 0, 0>(tb.U, tb, r);
 #pragma unroll
