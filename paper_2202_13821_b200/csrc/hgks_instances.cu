@@ -21,8 +21,7 @@ struct Launch {
         // staged coefficients of both neighbours (double-buffered by default)
         // [+ the flux accumulators when they live in shared memory]
         return (HGKS_FACE_STAGES * (2 * SH::NC * 32) +
-                (HGKS_FACE_ACC_SMEM == 1 ? 35 * FaceCTA<P, DIM, AXIS>::NT
-                 : HGKS_FACE_ACC_SMEM == 2 ? 15 * FaceCTA<P, DIM, AXIS>::NT : 0)) *
+                (HGKS_FACE_ACC_SMEM ? 35 * FaceCTA<P, DIM, AXIS>::NT : 0)) *
                (int)sizeof(double);
     }
     // persistent face kernels: resident CTAs on the whole GPU per axis

@@ -402,12 +402,8 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
             const double* cL = sc + lane;
             const double* cR = sc + NC * 32 + lane;
 
-#if HGKS_FACE_ACC_SMEM == 1
+#if HGKS_FACE_ACC_SMEM
             SmemAcc acc{smem + HGKS_FACE_STAGES * STG + tid, NT};
-#elif HGKS_FACE_ACC_SMEM == 2
-            HybridAcc acc;
-            acc.p = smem + HGKS_FACE_STAGES * STG + tid;
-            acc.stride = NT;
 #else
             FluxAcc acc;
 #endif

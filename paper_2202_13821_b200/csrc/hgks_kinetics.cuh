@@ -328,19 +328,6 @@ struct SmemAcc {
     HD double& nq(int k, int m) { return p[(20 + 5 * k + m) * stride]; }
 };
 
-// q0 and dq0 in registers, the non-equilibrium moments (touched once per side
-// and once in the merge) in a per-thread shared-memory column: 30 fewer
-// live registers through the side passes
-struct HybridAcc {
-    double q0_[5];
-    double dq0_[3][5];
-    double* p;   // &base[tid]
-    int stride;  // threads per CTA
-    HD double& q0(int m) { return q0_[m]; }
-    HD double& dq0(int d, int m) { return dq0_[d][m]; }
-    HD double& nq(int k, int m) { return p[(5 * k + m) * stride]; }
-};
-
 template <class Acc>
 HD void flux_init(Acc& acc) {
 #pragma unroll
