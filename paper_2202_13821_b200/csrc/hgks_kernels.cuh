@@ -622,10 +622,21 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
     };
     auto prefetch_coef = [&](const TI& ti, double* dst) {
         const long cbase = (long)(ti.k + 1) * kp.S + (long)ti.j * nx;
-        for (int e = tid; e < CT::COEF; e += NT) {
-            const int l = e % TC, comp = e / TC;
+        if constexpr (NT % TC == 0) {
+            // fixed column per thread, components strided by NT / TC
+            constexpr int CST = NT / TC;
+            const int l = tid % TC;
             const bool ok = ti.i0 + l < nx;
-            cp_async8(dst + comp * TC + l, qin + comp * kp.cs + cbase + (ok ? ti.i0 + l : 0), ok);
+            const double* src = qin + (long)(tid / TC) * kp.cs + cbase + (ok ? ti.i0 + l : 0);
+            const long sst = CST * kp.cs;
+#pragma unroll 4
+            for (int comp = tid / TC; comp < NC; comp += CST, src += sst) cp_async8(dst + comp * TC + l, src, ok);
+        } else {
+            for (int e = tid; e < CT::COEF; e += NT) {
+                const int l = e % TC, comp = e / TC;
+                const bool ok = ti.i0 + l < nx;
+                cp_async8(dst + comp * TC + l, qin + comp * kp.cs + cbase + (ok ? ti.i0 + l : 0), ok);
+            }
         }
     };
     // stage 2 consumes only the Ft rows (the face pass stores only those)
@@ -650,17 +661,23 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
             const bool ok = ig < nx;
             const long oy = (lane < TC ? rowk : rowp) + (ok ? ig : 0);
             const long oz = (lane < TC ? rowk : rowz) + (ok ? ig : 0);
-            for (int rr = warp; rr < CT::NFX * RW; rr += NW) {
-                const int r = face_row(rr);
-                if (lane <= TC) cp_async8(fx + r * (TC + 1) + lane, f0 + (long)r * kp.fs + ox, okx);
-            }
-            for (int rr = warp; rr < CT::NFY * RW; rr += NW) {
-                const int r = face_row(rr);
-                cp_async8(fy + r * 2 * TC + lane, f1 + (long)r * kp.fs + oy, ok);
-            }
-            for (int rr = warp; rr < CT::NFZ * RW; rr += NW) {
-                const int r = face_row(rr);
-                cp_async8(fz + r * 2 * TC + lane, f2 + (long)r * kp.fs + oz, ok);
+            // a warp owns component rows c (F/Ft x var) and walks the face
+            // points with constant strides: row pf*10 + RO + c
+            const long pst = 10 * kp.fs;
+            for (int c = warp; c < RW; c += NW) {
+                const int r0 = RO + c;
+                const double* sx = f0 + (long)r0 * kp.fs + ox;
+                const double* sy = f1 + (long)r0 * kp.fs + oy;
+                const double* sz = f2 + (long)r0 * kp.fs + oz;
+#pragma unroll
+                for (int pf = 0; pf < CT::NFX; ++pf)
+                    if (lane <= TC) cp_async8(fx + (pf * 10 + r0) * (TC + 1) + lane, sx + pf * pst, okx);
+#pragma unroll
+                for (int pf = 0; pf < CT::NFY; ++pf)
+                    cp_async8(fy + (pf * 10 + r0) * 2 * TC + lane, sy + pf * pst, ok);
+#pragma unroll
+                for (int pf = 0; pf < CT::NFZ; ++pf)
+                    cp_async8(fz + (pf * 10 + r0) * 2 * TC + lane, sz + pf * pst, ok);
             }
         } else {
             for (int e = tid; e < CT::NFX * RW * (TC + 1); e += NT) {  // x faces i0 .. i0+TC (periodic wrap at nx)
