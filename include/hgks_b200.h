@@ -148,6 +148,13 @@ int hgks_halo_unpack(hgks_solver* s, int which);
  * hgks_step fails; a single slab fills its ghosts by the periodic wrap. */
 typedef int (*hgks_halo_fn)(void* user, hgks_solver* s, int which);
 void hgks_set_halo_exchange(hgks_solver* s, hgks_halo_fn fn, void* user);
+/* Overlapped exchange (takes precedence over the single callback when both
+ * are set): start(user, s, which) runs right after the pack and must only
+ * ENQUEUE the transfer behind the solver stream; the faces that need no ghost
+ * layer (x and y faces of every owned layer, z faces of layers 1..nzl-1) are
+ * then launched, and finish(user, s, which) must make the solver stream wait
+ * for the transfer; unpack and the two boundary z-face layers follow. */
+void hgks_set_halo_exchange_split(hgks_solver* s, hgks_halo_fn start, hgks_halo_fn finish, void* user);
 /* Split-phase step for callers that drive the exchange themselves (several
  * slabs in one process): phase 0 = stage 1 (needs q^n ghosts), phase 1 =
  * stage 2 (needs q* ghosts), phase 2 = error check + commit. A single slab

@@ -27,7 +27,7 @@ EXPORTS = [
     "hgks_residual", "hgks_apply_inverse_mass", "hgks_compute_dt", "hgks_step",
     "hgks_two_stage_step_host", "hgks_two_stage_step_host_streamed", "hgks_advance", "hgks_set_count_fluxes", "hgks_flux_evaluations",
     "hgks_project_case", "hgks_tgv_diagnostics", "hgks_error_norms", "hgks_halo_bytes", "hgks_halo_buffers",
-    "hgks_halo_pack", "hgks_halo_unpack", "hgks_set_halo_exchange", "hgks_step_phase",
+    "hgks_halo_pack", "hgks_halo_unpack", "hgks_set_halo_exchange", "hgks_set_halo_exchange_split", "hgks_step_phase",
     "hgks_set_dt_reduce", "hgks_set_stream", "hgks_get_stream", "hgks_synchronize",
     "hgks_launch_count", "hgks_set_kernel_timing", "hgks_kernel_times", "hgks_measure_fp64_peak",
 ]
@@ -97,6 +97,8 @@ def load():
     L.hgks_measure_fp64_peak.argtypes = [ctypes.c_int, ctypes.c_double, _dp]
     L.hgks_set_halo_exchange.argtypes = [sp, HALO_FN, sp]
     L.hgks_set_halo_exchange.restype = None
+    L.hgks_set_halo_exchange_split.argtypes = [sp, HALO_FN, HALO_FN, sp]
+    L.hgks_set_halo_exchange_split.restype = None
     L.hgks_set_dt_reduce.argtypes = [sp, MIN_FN, sp]
     L.hgks_set_dt_reduce.restype = None
     L.hgks_set_stream.argtypes = [sp, sp]

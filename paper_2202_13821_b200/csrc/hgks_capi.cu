@@ -58,6 +58,8 @@ struct hgks_solver {
     // hooks
     hgks_halo_fn halo = nullptr;
     void* halo_user = nullptr;
+    hgks_halo_fn halo_start = nullptr, halo_finish = nullptr;  // overlapped exchange
+    void* halo_split_user = nullptr;
     hgks_min_fn dtmin = nullptr;
     void* dtmin_user = nullptr;
     double* d_halo = nullptr;  // [4][NC][S]: send_lo, send_hi, recv_lo, recv_hi
@@ -260,13 +262,34 @@ void ev_record(hgks_solver* s, int i) {
 int run_residual(hgks_solver* s, int which, double dt, int stage, int mode, const double* qn,
                  double* o0, double* o1, double* o2) {
     double* in = which_array(s, which);
-    int rc = fill_ghosts(s, which);
-    if (rc) return rc;
     KParams kp = make_params(s, dt, stage);
     kp.ft_only = mode == MODE_STAGE2;
-    ev_record(s, stage * 3 + 0);
-    s->ks.face(kp, in, s->face, s->stream, 0, nullptr);
-    s->launches += 3;
+    if (!s->single && !s->external_halo && s->halo_start) {
+        // overlapped halo: pack -> start the exchange -> faces that need no
+        // ghost (x, y faces of every owned layer, z faces of layers
+        // 1..nzl-1) -> finish -> unpack -> z faces of layers 0 and nzl
+        int rc = halo_pack(s, which);
+        if (rc) return rc;
+        if (s->halo_start(s->halo_split_user, s, which) != 0)
+            return fail(s, HGKS_ERR_CUDA, "halo exchange start callback failed");
+        ev_record(s, stage * 3 + 0);
+        s->ks.face_axis(kp, 0, in, s->face[0], s->stream, 0, s->nzl);
+        s->ks.face_axis(kp, 1, in, s->face[1], s->stream, 0, s->nzl);
+        s->ks.face_axis(kp, 2, in, s->face[2], s->stream, 1, s->nzl);
+        if (s->halo_finish(s->halo_split_user, s, which) != 0)
+            return fail(s, HGKS_ERR_CUDA, "halo exchange finish callback failed");
+        rc = halo_unpack(s, which);
+        if (rc) return rc;
+        s->ks.face_axis(kp, 2, in, s->face[2], s->stream, 0, 1);
+        s->ks.face_axis(kp, 2, in, s->face[2], s->stream, s->nzl, kp.zface_layers);
+        s->launches += 5;
+    } else {
+        int rc = fill_ghosts(s, which);
+        if (rc) return rc;
+        ev_record(s, stage * 3 + 0);
+        s->ks.face(kp, in, s->face, s->stream, 0, nullptr);
+        s->launches += 3;
+    }
     ev_record(s, stage * 3 + 1);
     s->ks.cell(kp, mode, in, s->face, qn, s->A, nullptr, o0, o1, o2, s->stream, 0, nullptr);
     s->launches += 1;
@@ -881,6 +904,12 @@ int hgks_step_phase(hgks_solver* s, double dt, int phase) {
 void hgks_set_halo_exchange(hgks_solver* s, hgks_halo_fn fn, void* user) {
     s->halo = fn;
     s->halo_user = user;
+}
+
+void hgks_set_halo_exchange_split(hgks_solver* s, hgks_halo_fn start, hgks_halo_fn finish, void* user) {
+    s->halo_start = start && finish ? start : nullptr;
+    s->halo_finish = start && finish ? finish : nullptr;
+    s->halo_split_user = user;
 }
 
 void hgks_set_dt_reduce(hgks_solver* s, hgks_min_fn fn, void* user) {

@@ -63,6 +63,12 @@ struct Launch {
         face_kernel<P, DIM, VISC, AXIS><<<grid, FaceCTA<P, DIM, AXIS>::NT, face_smem<AXIS>(), st>>>(
             kp, q, f, first, count, 0);
     }
+    static void face_axis_range(const KParams& kp, int axis, const double* q, double* f, cudaStream_t st,
+                                int kb, int ke) {
+        if (axis == 0) face_axis_layers<0>(kp, q, f, st, kb, ke);
+        else if (axis == 1) face_axis_layers<1>(kp, q, f, st, kb, ke);
+        else face_axis_layers<2>(kp, q, f, st, kb, ke);
+    }
     static void face_layers(const KParams& kp, const double* q, double* const f[3], cudaStream_t st,
                             int kb, int ke) {
         face_axis_layers<0>(kp, q, f[0], st, kb, ke);
@@ -155,6 +161,7 @@ struct Launch {
         k.face = &face;
         k.cell = &cell;
         k.face_layers = &face_layers;
+        k.face_axis = &face_axis_range;
         k.cell_layers = &cell_layers;
         k.face_smem[0] = face_smem<0>();
         k.face_smem[1] = face_smem<1>();

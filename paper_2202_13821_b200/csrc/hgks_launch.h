@@ -18,6 +18,10 @@ struct KernelSet {
     // axes / the cell update of those layers), for the streamed host step
     void (*face_layers)(const KParams&, const double* q, double* const f[3], cudaStream_t, int kb,
                         int ke);
+    // one face axis over z layers [kb, ke) (z: up to zface_layers), for the
+    // multi-slab step that overlaps the halo exchange with interior faces
+    void (*face_axis)(const KParams&, int axis, const double* q, double* f, cudaStream_t, int kb,
+                      int ke);
     void (*cell_layers)(const KParams&, int mode, const double* qin, double* const f[3],
                         const double* qn, const double* L1, const double* Lt1, double* o0,
                         double* o1, double* o2, cudaStream_t, int kb, int ke);

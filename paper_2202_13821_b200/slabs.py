@@ -12,7 +12,10 @@ independent, exact).
 Transport is torch.distributed (NCCL on GPUs, gloo on CPU for tests): the
 solver packs its boundary layers into contiguous device buffers
 (hgks_halo_pack), this module moves them, the solver unpacks
-(hgks_halo_unpack) — all on one stream.
+(hgks_halo_unpack). The exchange is split (hgks_set_halo_exchange_split):
+it is enqueued right after the pack, the faces that need no ghost layer run
+while the layers are in flight, and the solver stream waits for the transfer
+only before the unpack and the two boundary z-face layers.
 """
 from __future__ import annotations
 
@@ -87,6 +90,32 @@ def exchange_halos(send_lo, send_hi, recv_lo, recv_hi, rank: int, world: int, gr
         w.wait()
 
 
+def start_halos(send_lo, send_hi, recv_lo, recv_hi, rank: int, world: int, group=None):
+    """Enqueue the exchange (NCCL: behind the current stream, on its own
+    stream) and return the pending work; finish_halos() makes the current
+    stream wait for it. Same posting order as exchange_halos."""
+    import torch.distributed as dist
+
+    if world == 1 or (send_lo.is_cuda and dist.get_backend(group) == "gloo"):
+        return None  # nothing to overlap: finish_halos does the whole exchange
+    lower, upper = ring_neighbors(rank, world)
+    ops = [
+        dist.P2POp(dist.isend, send_lo, lower, group, 0),
+        dist.P2POp(dist.irecv, recv_hi, upper, group, 0),
+        dist.P2POp(dist.isend, send_hi, upper, group, 1),
+        dist.P2POp(dist.irecv, recv_lo, lower, group, 1),
+    ]
+    return dist.batch_isend_irecv(ops)
+
+
+def finish_halos(pending, send_lo, send_hi, recv_lo, recv_hi, rank: int, world: int, group=None):
+    if pending is None:
+        exchange_halos(send_lo, send_hi, recv_lo, recv_hi, rank, world, group)
+        return
+    for w in pending:
+        w.wait()
+
+
 def min_allreduce(value: float, device: Optional[str] = None, group=None) -> float:
     import torch
     import torch.distributed as dist
@@ -121,22 +150,32 @@ def attach(solver, rank: int, world: int, device: int, group=None):
     ptrs = solver.halo_buffers()
     views = [device_view(p, nbytes, device) for p in ptrs]
 
-    def exchange(_s, _which):
-        # the pack kernel ran on the solver's stream; torch's copies / NCCL ops
-        # run on torch's current stream. When they are not the same stream,
-        # order them explicitly (stream 0 is the legacy default stream, never
-        # the solver's).
+    def same_stream():
+        # the pack kernel runs on the solver's stream; torch's copies / NCCL ops
+        # order against torch's current stream. When they are not the same
+        # stream, order them explicitly (stream 0 is the legacy default
+        # stream, never the solver's).
         ts = torch.cuda.current_stream(device)
-        same = ts.cuda_stream != 0 and ts.cuda_stream == solver.stream()
+        return ts, ts.cuda_stream != 0 and ts.cuda_stream == solver.stream()
+
+    pending = {}
+
+    def start(_s, which):
+        ts, same = same_stream()
         if not same:
             solver.synchronize()
-        exchange_halos(views[0], views[1], views[2], views[3], rank, world, group)
+        pending[which] = start_halos(views[0], views[1], views[2], views[3], rank, world, group)
+
+    def finish(_s, which):
+        ts, same = same_stream()
+        finish_halos(pending.pop(which, None), views[0], views[1], views[2], views[3], rank, world, group)
         if not same:
             ts.synchronize()
 
     import torch.distributed as dist
 
     red_dev = "cpu" if dist.get_backend(group) == "gloo" else f"cuda:{device}"
-    solver.set_halo_exchange(exchange)
+    # interior faces run while the layers are in flight
+    solver.set_halo_exchange_split(start, finish)
     solver.set_dt_reduce(lambda v: min_allreduce(v, device=red_dev, group=group))
     return views

@@ -371,6 +371,25 @@ class Solver:
         self._cbs.append(c)
         self.L.hgks_set_halo_exchange(self.h, c, None)
 
+    def set_halo_exchange_split(self, start: Callable[["Solver", int], None],
+                                finish: Callable[["Solver", int], None]):
+        """Overlapped exchange: start(solver, which) enqueues the transfer
+        behind the solver stream, the ghost-free faces are launched, then
+        finish(solver, which) makes the solver stream wait for it."""
+        def wrap(fn):
+            def cb(user, h, which):
+                try:
+                    fn(self, which)
+                    return 0
+                except Exception:  # noqa: BLE001 — reported as an ABI failure
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+            return _lib.HALO_FN(cb)
+        a, b = wrap(start), wrap(finish)
+        self._cbs += [a, b]
+        self.L.hgks_set_halo_exchange_split(self.h, a, b, None)
+
     def set_dt_reduce(self, fn: Callable[[float], float]):
         def cb(user, val):
             try:
