@@ -573,7 +573,8 @@ struct CellTile {
     static constexpr int FZ = NFZ * 10 * 2 * TC;   // z faces layers k, k+1
     static constexpr int VF = NVP * 30 * TC;       // volume-point fluxes [p][30][TC]
     static constexpr int LB = 2 * NC * TC;         // L, Lt of the tile (stage-1 q*)
-    static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + LB;
+    static constexpr int GEO = 2 * TC + 4;          // widths of a tile: dx, 2/dx [TC]; dy, dz, 2/dy, 2/dz
+    static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + LB + 2 * GEO;
 };
 
 // Persistent CTA over tiles of TC consecutive cells along x, software
@@ -602,6 +603,7 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
     double* fz = fy + CT::FY;
     double* vf = fz + CT::FZ;             // [NVP][30][TC]
     double* lb = vf + CT::VF;             // [2][NC][TC]
+    double* geob = lb + CT::LB;           // [2][GEO], staged with the coefficients
 
     const int tid = threadIdx.x;
     const int nx = kp.nx, ny = kp.ny;
@@ -620,8 +622,21 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
         r.j = a - r.k * ny;
         return r;
     };
-    auto prefetch_coef = [&](const TI& ti, double* dst) {
+    auto prefetch_coef = [&](const TI& ti, double* dst, double* gdst) {
         const long cbase = (long)(ti.k + 1) * kp.S + (long)ti.j * nx;
+        // the tile's widths ride along (loaded through the async copy so their
+        // latency is hidden like the coefficients')
+        if (tid < TC) {
+            const bool ok = ti.i0 + tid < nx;
+            const int i = ok ? ti.i0 + tid : 0;
+            cp_async8(gdst + tid, kp.dx + i, ok);
+            cp_async8(gdst + TC + tid, kp.i2dx + i, ok);
+        } else if (tid < TC + 4) {
+            const int r = tid - TC;
+            const double* src = r == 0 ? kp.dy + ti.j : r == 1 ? kp.dz + ti.k + 1 : r == 2 ? kp.i2dy + ti.j
+                                                                                          : kp.i2dz + ti.k + 1;
+            cp_async8(gdst + 2 * TC + r, src, true);
+        }
         if constexpr (NT % TC == 0) {
             // fixed column per thread, components strided by NT / TC
             constexpr int CST = NT / TC;
@@ -701,30 +716,10 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
             }
         }
     };
-    // every item of this thread is cell lt of the tile (NT % TC == 0), so its
-    // widths are loaded one tile ahead into registers
-    static_assert(NT % TC == 0, "cell items must keep their column");
-    const int lt = tid % TC;
-    struct Geo {
-        double hx, i2hx, hy, hz, i2hy, i2hz;
-    };
-    auto geo_of = [&](const TI& ti) {
-        const int i = ti.i0 + lt < nx ? ti.i0 + lt : 0;
-        Geo g;
-        g.hx = __ldg(kp.dx + i);
-        g.i2hx = __ldg(kp.i2dx + i);
-        g.hy = __ldg(kp.dy + ti.j);
-        g.hz = __ldg(kp.dz + ti.k + 1);
-        g.i2hy = __ldg(kp.i2dy + ti.j);
-        g.i2hz = __ldg(kp.i2dz + ti.k + 1);
-        return g;
-    };
-
     const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
     TI cur = tile_of(t0);
-    if (t0 < tile_end) prefetch_coef(cur, coefb);
+    if (t0 < tile_end) prefetch_coef(cur, coefb, geob);
     cp_async_commit();
-    Geo gcur = t0 < tile_end ? geo_of(cur) : Geo{};
     const double dt = kp.dt;
     int n = 0;
     for (int t = t0; t < tile_end; t += step, ++n) {
@@ -733,23 +728,23 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
         cp_async_commit();
         const bool has_next = t + step < tile_end;
         const TI nxt = has_next ? tile_of(t + step) : cur;
-        if (has_next) prefetch_coef(nxt, coefb + ((n + 1) & 1) * CT::COEF);
+        if (has_next) prefetch_coef(nxt, coefb + ((n + 1) & 1) * CT::COEF, geob + ((n + 1) & 1) * CT::GEO);
         cp_async_commit();
-        const Geo gnxt = geo_of(nxt);
         const int i0 = cur.i0, j = cur.j, k = cur.k;
         const long cbase = (long)(k + 1) * kp.S + (long)j * nx;
-        const double hy = gcur.hy, hz = gcur.hz;
-        const double i2hy = gcur.i2hy, i2hz = gcur.i2hz;
+        const double* gg = geob + (n & 1) * CT::GEO;
         const long cglob_row = (long)nx * (j + (long)ny * (k + kp.kglob0));
-        cp_async_wait<2>();  // this tile's coefficients
+        cp_async_wait<2>();  // this tile's coefficients and widths
         __syncthreads();
+        const double hy = gg[2 * TC], hz = gg[2 * TC + 1];
+        const double i2hy = gg[2 * TC + 2], i2hz = gg[2 * TC + 3];
 
         // ---- phase B: smooth fluxes at volume points
         for (int it = tid; it < TC * NVP; it += NT) {
             const int l = it % TC, p = it / TC;
             const int i = i0 + l;
             if (i >= nx) continue;
-            const double i2h[3] = {gcur.i2hx, i2hy, i2hz};
+            const double i2h[3] = {gg[TC + l], i2hy, i2hz};
             double e[20];
             if constexpr (SH::NQ == 2) vol_eval_sym<P, DIM, TC>(p, sc + l, i2h, e);
             else vol_eval_rt<P, DIM, TC, NVP>(p, sc + l, i2h, e);
@@ -776,8 +771,8 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
             const int v = vv % 5, ft = FT0 + vv / 5;  // ft: 0 -> F (R), 1 -> Ft (Rt)
             const int i = i0 + l;
             if (i >= nx) continue;
-            const double hx = gcur.hx;
-            const double i2h[3] = {gcur.i2hx, i2hy, i2hz};
+            const double hx = gg[l];
+            const double i2h[3] = {gg[TC + l], i2hy, i2hz};
             const int row = 5 * ft + v;
             double R[N];
 #pragma unroll
@@ -875,7 +870,6 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
         }
         __syncthreads();  // buffers of this tile are free for the next prefetch
         cur = nxt;
-        gcur = gnxt;
     }
     cp_async_wait<0>();
 }
