@@ -125,113 +125,71 @@ __device__ __forceinline__ void report_error(const KParams& kp, unsigned long lo
 
 // -------------------------------------------------------------- face kernel
 
-// Trace of one side at face point PT in the face-local frame
-// (eval_tabulated dg.hpp:139-161 + to_face_local dg.hpp:323-334).
-// SIDE 0 = minus-side cell at its plus face (ref coord +1), 1 = plus-side
-// cell at its minus face (-1). c = smem coefficients [comp][32] of the cell.
-template <int P, int DIM, int AXIS, int PT, int SIDE>
-__device__ __forceinline__ void face_trace(const double* __restrict__ c, const double* i2h,
-                                           double* t) {
-    using SH = Shape<P, DIM>;
-    constexpr int N = SH::N, NQ = SH::NQ;
-    constexpr double s = SIDE == 0 ? 1.0 : -1.0;
-    constexpr int C1 = (AXIS + 1) % 3, C2 = (AXIS + 2) % 3;
-    double e[20];
-#pragma unroll
-    for (int m = 0; m < 20; ++m) e[m] = 0.0;
-#pragma unroll
-    for (int n = 0; n < N; ++n) {
-        const double b = ctab<P, DIM>.fB[AXIS][SIDE == 0 ? 1 : 0][PT][n];
-        const double d0 = ctab<P, DIM>.fdB[AXIS][SIDE == 0 ? 1 : 0][PT][0][n];
-        const double d1 = ctab<P, DIM>.fdB[AXIS][SIDE == 0 ? 1 : 0][PT][1][n];
-        const double d2 = ctab<P, DIM>.fdB[AXIS][SIDE == 0 ? 1 : 0][PT][2][n];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-            const double cv = c[(n * 5 + v) * 32];
-            if (b != 0.0) e[v] += b * cv;
-            if (d0 != 0.0) e[5 + v] += d0 * cv;
-            if (d1 != 0.0) e[10 + v] += d1 * cv;
-            if (d2 != 0.0) e[15 + v] += d2 * cv;
-        }
-    }
-    // global -> face-local: momentum and derivative directions cycled to
-    // (AXIS, C1, C2); derivatives scaled by 2/h of their direction
-    constexpr int g[3] = {AXIS, C1, C2};
-    t[0] = e[0];
-    t[1] = e[1 + AXIS];
-    t[2] = e[1 + C1];
-    t[3] = e[1 + C2];
-    t[4] = e[4];
-#pragma unroll
-    for (int d = 1; d < 4; ++d) {
-        const int gd = g[d - 1];
-        const double* src = e + 5 + 5 * gd;
-        const double sf = i2h[gd];
-        t[5 * d + 0] = sf * src[0];
-        t[5 * d + 1] = sf * src[1 + AXIS];
-        t[5 * d + 2] = sf * src[1 + C1];
-        t[5 * d + 3] = sf * src[1 + C2];
-        t[5 * d + 4] = sf * src[4];
-    }
-}
-
-// runtime point index -> compile-time instantiation (warp-uniform branch)
-template <int P, int DIM, int AXIS, int NFP, int PT = 0>
-__device__ __forceinline__ void face_trace_rt(int p, int side, const double* c, const double* i2h,
-                                              double* t) {
-    if constexpr (PT < NFP) {
-        if (p == PT) {
-            if (side == 0) face_trace<P, DIM, AXIS, PT, 0>(c, i2h, t);
-            else face_trace<P, DIM, AXIS, PT, 1>(c, i2h, t);
-        } else {
-            face_trace_rt<P, DIM, AXIS, NFP, PT + 1>(p, side, c, i2h, t);
-        }
-    }
-}
-
-// ---- sign symmetry of the 2-point Gauss rule (P1/P2)
-// The rule's abscissae are +-g on every axis and P_l(-x) = (-1)^l P_l(x)
-// exactly in floating point, so a table row at point p equals the row at the
-// all-positive point with basis n negated by prod_a s_a^{par_a(n)} (a
-// derivative along axis a carries one more s_a). Flipping the sign bit of
-// the coefficient (an integer op) instead of instantiating one evaluator per
-// point gives a single code path for every point and bitwise the same
-// products and sums; the symmetry of the tables is checked at compile time.
+// ---- sign symmetry of the tensor Gauss rules
+// Per axis the rule's abscissae are symmetric (-g, [0,] +g) and
+// P_l(-x) = (-1)^l P_l(x) exactly in floating point. A quadrature point's
+// CLASS is its zero pattern (which coordinates are 0: the middle point of the
+// 3-point rule, or a collapsed 2-D axis); within a class a table row equals
+// the row at the class' canonical point (+g on every non-zero axis) with
+// basis n negated by prod over negative axes of (-1)^{par_a(n)} (a derivative
+// along a negative axis carries one more sign). The evaluators below flip
+// the sign bit of each coefficient (an integer op) and run ONE compile-time
+// table per class: 1 class for the 2-point rule, 4 face / 8 volume classes
+// for the 3-point rule (instead of one code path per point: 9 / 27 for P3).
+// The products and sums are bitwise those of the per-point tables; the
+// symmetry of the tables is verified at compile time (gauss_symmetric).
 constexpr unsigned kSignBit = 0x80000000u;
 __device__ __forceinline__ double flip_sign(double x, unsigned m) {
     return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
 }
+__host__ __device__ constexpr bool g_zero(int nq, int idx) { return (nq & 1) && idx == nq / 2; }
+__host__ __device__ constexpr bool g_neg(int nq, int idx) { return !g_zero(nq, idx) && idx < nq / 2; }
+__host__ __device__ constexpr int g_canon(int nq, int idx) { return g_zero(nq, idx) ? idx : nq - 1; }
+
+// face-point geometry of axis a: tangential axes (C1, C2) with nb, nc points
+template <int P, int DIM, int AXIS>
+struct FaceRule {
+    static constexpr int NQ = Shape<P, DIM>::NQ;
+    static constexpr int C1 = (AXIS + 1) % 3, C2 = (AXIS + 2) % 3;
+    static constexpr int NB = (C1 == 2 && DIM == 2) ? 1 : NQ;
+    static constexpr int NCC = (C2 == 2 && DIM == 2) ? 1 : NQ;
+    // class = (tangential 1 zero, tangential 2 zero) -> canonical point
+    static constexpr int canon(int zb, int zc) {
+        return (zb ? NB / 2 : NB - 1) * NCC + (zc ? NCC / 2 : NCC - 1);
+    }
+};
 
 template <int P, int DIM>
-constexpr bool gauss2_symmetric() {
+constexpr bool gauss_symmetric() {
     constexpr ct::Tab T = ct::make_tab<P, DIM>();
-    const int nqz = DIM == 3 ? 2 : 1;
+    const int NQ = T.NQ, nqz = DIM == 3 ? NQ : 1;
     auto sg = [](bool neg, int par) { return (neg && par) ? -1.0 : 1.0; };
-    // volume points p = (i*2 + j)*nqz + k; canonical p* = NVP - 1
     for (int p = 0; p < T.NVP; ++p) {
-        const bool ni = p / (2 * nqz) == 0, nj = (p / nqz) % 2 == 0, nk = nqz == 2 && p % nqz == 0;
+        const int i = p / (NQ * nqz), j = (p / nqz) % NQ, k = p % nqz;
+        const bool ni = g_neg(NQ, i), nj = g_neg(NQ, j), nk = g_neg(nqz, k);
+        const int pc = (g_canon(NQ, i) * NQ + g_canon(NQ, j)) * nqz + g_canon(nqz, k);
         for (int n = 0; n < T.N; ++n) {
             const double sn = sg(ni, T.par[0][n]) * sg(nj, T.par[1][n]) * sg(nk, T.par[2][n]);
-            if (T.vB[p][n] != sn * T.vB[T.NVP - 1][n]) return false;
+            if (T.vB[p][n] != sn * T.vB[pc][n]) return false;
             const double sa[3] = {ni ? -1.0 : 1.0, nj ? -1.0 : 1.0, nk ? -1.0 : 1.0};
             for (int a = 0; a < 3; ++a)
-                if (T.vdB[p][a][n] != sa[a] * sn * T.vdB[T.NVP - 1][a][n]) return false;
+                if (T.vdB[p][a][n] != sa[a] * sn * T.vdB[pc][a][n]) return false;
         }
     }
-    // face points p = ib * nc + ic over the tangential axes (C1, C2)
     for (int a = 0; a < 3; ++a) {
         const int c1 = (a + 1) % 3, c2 = (a + 2) % 3;
-        const int nb = (c1 == 2 && DIM == 2) ? 1 : 2, nc = (c2 == 2 && DIM == 2) ? 1 : 2;
-        const int ps = (nb - 1) * nc + (nc - 1);
+        const int nb = (c1 == 2 && DIM == 2) ? 1 : NQ, nc = (c2 == 2 && DIM == 2) ? 1 : NQ;
         for (int sd = 0; sd < 2; ++sd)
             for (int p = 0; p < nb * nc; ++p) {
-                const bool n1 = nb == 2 && p / nc == 0, n2 = nc == 2 && p % nc == 0;
+                const int ib = p / nc, ic = p % nc;
+                const bool n1 = g_neg(nb, ib), n2 = g_neg(nc, ic);
+                const int pc = g_canon(nb, ib) * nc + g_canon(nc, ic);
                 for (int n = 0; n < T.N; ++n) {
                     const double sn = sg(n1, T.par[c1][n]) * sg(n2, T.par[c2][n]);
-                    if (T.fB[a][sd][p][n] != sn * T.fB[a][sd][ps][n]) return false;
+                    if (T.fB[a][sd][p][n] != sn * T.fB[a][sd][pc][n]) return false;
                     for (int d = 0; d < 3; ++d) {
-                        const double sd1 = d == c1 && n1 ? -1.0 : 1.0, sd2 = d == c2 && n2 ? -1.0 : 1.0;
-                        if (T.fdB[a][sd][p][d][n] != sd1 * sd2 * sn * T.fdB[a][sd][ps][d][n]) return false;
+                        const double s1 = d == c1 && n1 ? -1.0 : 1.0, s2 = d == c2 && n2 ? -1.0 : 1.0;
+                        if (T.fdB[a][sd][p][d][n] != s1 * s2 * sn * T.fdB[a][sd][pc][d][n]) return false;
                     }
                 }
             }
@@ -239,20 +197,18 @@ constexpr bool gauss2_symmetric() {
     return true;
 }
 
-// face_trace for the 2-point rule: one code path for all face points
-template <int P, int DIM, int AXIS, int SIDE>
-__device__ __forceinline__ void face_trace_sym(int p, const double* __restrict__ c, const double* i2h,
-                                               double* t) {
+// Trace of one side at a face point of class PS (its canonical index) in the
+// face-local frame (eval_tabulated dg.hpp:139-161 + to_face_local
+// dg.hpp:323-334); m1, m2: sign masks of the point's tangential axes.
+// SIDE 0 = minus-side cell at its plus face (ref coord +1), 1 = plus-side
+// cell at its minus face (-1). c = shared-memory coefficients [comp][RS].
+template <int P, int DIM, int AXIS, int SIDE, int RS, int PS>
+__device__ __forceinline__ void face_trace_canon(unsigned m1, unsigned m2, const double* __restrict__ c,
+                                                 const double* i2h, double* t) {
     using SH = Shape<P, DIM>;
-    static_assert(SH::NQ == 2, "sign-symmetric traces need the 2-point rule");
-    static_assert(gauss2_symmetric<P, DIM>(), "basis tables are not sign-symmetric");
     constexpr int N = SH::N;
     constexpr int C1 = (AXIS + 1) % 3, C2 = (AXIS + 2) % 3;
-    constexpr int NB = (C1 == 2 && DIM == 2) ? 1 : 2, NCC = (C2 == 2 && DIM == 2) ? 1 : 2;
-    constexpr int PS = (NB - 1) * NCC + (NCC - 1);
     constexpr int SI = SIDE == 0 ? 1 : 0;
-    const unsigned m1 = (NB == 2 && p / NCC == 0) ? kSignBit : 0u;
-    const unsigned m2 = (NCC == 2 && p % NCC == 0) ? kSignBit : 0u;
     double e[20];
 #pragma unroll
     for (int m = 0; m < 20; ++m) e[m] = 0.0;
@@ -265,13 +221,16 @@ __device__ __forceinline__ void face_trace_sym(int p, const double* __restrict__
         const unsigned mn = (ctab<P, DIM>.par[C1][n] ? m1 : 0u) ^ (ctab<P, DIM>.par[C2][n] ? m2 : 0u);
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
-            const double cv = flip_sign(c[(n * 5 + v) * 32], mn);
+            const double cv = flip_sign(c[(n * 5 + v) * RS], mn);
             if (b != 0.0) e[v] += b * cv;
             if (d0 != 0.0) e[5 + v] += d0 * cv;
             if (d1 != 0.0) e[10 + v] += d1 * cv;
             if (d2 != 0.0) e[15 + v] += d2 * cv;
         }
     }
+    // global -> face-local: momentum and derivative directions cycled to
+    // (AXIS, C1, C2); derivatives scaled by 2/h of their direction (with the
+    // point's sign on a tangential axis)
     constexpr int g[3] = {AXIS, C1, C2};
     t[0] = e[0];
     t[1] = e[1 + AXIS];
@@ -282,13 +241,31 @@ __device__ __forceinline__ void face_trace_sym(int p, const double* __restrict__
     for (int d = 1; d < 4; ++d) {
         const int gd = g[d - 1];
         const double* src = e + 5 + 5 * gd;
-        // derivative along a tangential axis carries that axis' point sign
         const double sf = flip_sign(i2h[gd], gd == C1 ? m1 : gd == C2 ? m2 : 0u);
         t[5 * d + 0] = sf * src[0];
         t[5 * d + 1] = sf * src[1 + AXIS];
         t[5 * d + 2] = sf * src[1 + C1];
         t[5 * d + 3] = sf * src[1 + C2];
         t[5 * d + 4] = sf * src[4];
+    }
+}
+
+// face point p -> its class' evaluator (one code path per class)
+template <int P, int DIM, int AXIS, int SIDE, int RS>
+__device__ __forceinline__ void face_trace_sym(int p, const double* __restrict__ c, const double* i2h,
+                                               double* t) {
+    static_assert(gauss_symmetric<P, DIM>(), "basis tables are not sign-symmetric");
+    using FR = FaceRule<P, DIM, AXIS>;
+    const int ib = p / FR::NCC, ic = p % FR::NCC;
+    const unsigned m1 = g_neg(FR::NB, ib) ? kSignBit : 0u, m2 = g_neg(FR::NCC, ic) ? kSignBit : 0u;
+    const bool zb = g_zero(FR::NB, ib), zc = g_zero(FR::NCC, ic);
+    if constexpr (FR::NQ == 2 && FR::NB != 1 && FR::NCC != 1) {
+        face_trace_canon<P, DIM, AXIS, SIDE, RS, FR::canon(0, 0)>(m1, m2, c, i2h, t);
+    } else {
+        if (!zb && !zc) face_trace_canon<P, DIM, AXIS, SIDE, RS, FR::canon(0, 0)>(m1, m2, c, i2h, t);
+        else if (!zb) face_trace_canon<P, DIM, AXIS, SIDE, RS, FR::canon(0, 1)>(m1, m2, c, i2h, t);
+        else if (!zc) face_trace_canon<P, DIM, AXIS, SIDE, RS, FR::canon(1, 0)>(m1, m2, c, i2h, t);
+        else face_trace_canon<P, DIM, AXIS, SIDE, RS, FR::canon(1, 1)>(m1, m2, c, i2h, t);
     }
 }
 
@@ -415,12 +392,8 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
 #pragma unroll 1
             for (int side = 0; side < 2 && !fail; ++side) {
                 double tr[20];
-                if constexpr (SH::NQ == 2) {
-                    if (side == 0) face_trace_sym<P, DIM, AXIS, 0>(p, cL, i2hL, tr);
-                    else face_trace_sym<P, DIM, AXIS, 1>(p, cR, i2hR, tr);
-                } else {
-                    face_trace_rt<P, DIM, AXIS, NFP>(p, side, side == 0 ? cL : cR, side == 0 ? i2hL : i2hR, tr);
-                }
+                if (side == 0) face_trace_sym<P, DIM, AXIS, 0, 32>(p, cL, i2hL, tr);
+                else face_trace_sym<P, DIM, AXIS, 1, 32>(p, cR, i2hR, tr);
                 double bad = 0.0, ps = 0.0;
                 const int rc = flux_side<VISC>(tr, side, kp.gas, acc, ps, bad);
                 psum += ps;
@@ -479,51 +452,13 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
 // -------------------------------------------------------------- cell kernel
 enum : int { MODE_RESIDUAL = 0, MODE_STAGE1 = 1, MODE_STAGE2 = 2 };
 
-// value + global derivatives at volume point PT (eval_tabulated, dg.hpp:139-161)
-template <int P, int DIM, int PT, int TC>
-__device__ __forceinline__ void vol_eval(const double* __restrict__ c, const double* i2h,
-                                         double* e) {
+// value + global derivatives at a volume point of class PS (canonical index)
+// (eval_tabulated, dg.hpp:139-161); m0..m2: the point's sign masks
+template <int P, int DIM, int TC, int PS>
+__device__ __forceinline__ void vol_eval_canon(unsigned m0, unsigned m1, unsigned m2,
+                                               const double* __restrict__ c, const double* i2h, double* e) {
     using SH = Shape<P, DIM>;
-    constexpr int N = SH::N, NQ = SH::NQ;
-#pragma unroll
-    for (int m = 0; m < 20; ++m) e[m] = 0.0;
-#pragma unroll
-    for (int n = 0; n < N; ++n) {
-        const double b = ctab<P, DIM>.vB[PT][n];
-        const double d0 = ctab<P, DIM>.vdB[PT][0][n];
-        const double d1 = ctab<P, DIM>.vdB[PT][1][n];
-        const double d2 = ctab<P, DIM>.vdB[PT][2][n];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-            const double cv = c[(n * 5 + v) * TC];
-            if (b != 0.0) e[v] += b * cv;
-            if (d0 != 0.0) e[5 + v] += d0 * cv;
-            if (d1 != 0.0) e[10 + v] += d1 * cv;
-            if (d2 != 0.0) e[15 + v] += d2 * cv;
-        }
-    }
-#pragma unroll
-    for (int v = 0; v < 5; ++v) {
-        e[5 + v] *= i2h[0];
-        e[10 + v] *= i2h[1];
-        e[15 + v] *= i2h[2];
-    }
-}
-
-// vol_eval for the 2-point rule: one code path for all volume points
-// (sign symmetry, see face_trace_sym)
-template <int P, int DIM, int TC>
-__device__ __forceinline__ void vol_eval_sym(int p, const double* __restrict__ c, const double* i2h,
-                                             double* e) {
-    using SH = Shape<P, DIM>;
-    static_assert(SH::NQ == 2, "sign-symmetric evaluation needs the 2-point rule");
-    static_assert(gauss2_symmetric<P, DIM>(), "basis tables are not sign-symmetric");
-    constexpr int N = SH::N, NVP = SH::NVP;
-    constexpr int NQZ = DIM == 3 ? 2 : 1;
-    constexpr int PS = NVP - 1;
-    const unsigned m0 = p / (2 * NQZ) == 0 ? kSignBit : 0u;
-    const unsigned m1 = (p / NQZ) % 2 == 0 ? kSignBit : 0u;
-    const unsigned m2 = (NQZ == 2 && p % NQZ == 0) ? kSignBit : 0u;
+    constexpr int N = SH::N;
 #pragma unroll
     for (int m = 0; m < 20; ++m) e[m] = 0.0;
 #pragma unroll
@@ -552,13 +487,56 @@ __device__ __forceinline__ void vol_eval_sym(int p, const double* __restrict__ c
     }
 }
 
-template <int P, int DIM, int TC, int NVP, int PT = 0>
-__device__ __forceinline__ void vol_eval_rt(int p, const double* c, const double* i2h, double* e) {
-    if constexpr (PT < NVP) {
-        if (p == PT) vol_eval<P, DIM, PT, TC>(c, i2h, e);
-        else vol_eval_rt<P, DIM, TC, NVP, PT + 1>(p, c, i2h, e);
+// volume point p = (i, j, k), k fastest -> its class' evaluator
+template <int P, int DIM, int TC>
+__device__ __forceinline__ void vol_eval_sym(int p, const double* __restrict__ c, const double* i2h,
+                                             double* e) {
+    static_assert(gauss_symmetric<P, DIM>(), "basis tables are not sign-symmetric");
+    constexpr int NQ = Shape<P, DIM>::NQ, NQZ = DIM == 3 ? NQ : 1;
+    const int i = p / (NQ * NQZ), j = (p / NQZ) % NQ, k = p % NQZ;
+    const unsigned m0 = g_neg(NQ, i) ? kSignBit : 0u, m1 = g_neg(NQ, j) ? kSignBit : 0u,
+                   m2 = g_neg(NQZ, k) ? kSignBit : 0u;
+    constexpr auto PC = [](int zi, int zj, int zk) {
+        return ((zi ? NQ / 2 : NQ - 1) * NQ + (zj ? NQ / 2 : NQ - 1)) * NQZ + (zk ? NQZ / 2 : NQZ - 1);
+    };
+    if constexpr (NQ == 2) {
+        vol_eval_canon<P, DIM, TC, PC(0, 0, 0)>(m0, m1, m2, c, i2h, e);
+    } else {
+        const int cls = (g_zero(NQ, i) ? 4 : 0) | (g_zero(NQ, j) ? 2 : 0) | (g_zero(NQZ, k) ? 1 : 0);
+        switch (cls) {
+            case 0: vol_eval_canon<P, DIM, TC, PC(0, 0, 0)>(m0, m1, m2, c, i2h, e); break;
+            case 1: vol_eval_canon<P, DIM, TC, PC(0, 0, 1)>(m0, m1, m2, c, i2h, e); break;
+            case 2: vol_eval_canon<P, DIM, TC, PC(0, 1, 0)>(m0, m1, m2, c, i2h, e); break;
+            case 3: vol_eval_canon<P, DIM, TC, PC(0, 1, 1)>(m0, m1, m2, c, i2h, e); break;
+            case 4: vol_eval_canon<P, DIM, TC, PC(1, 0, 0)>(m0, m1, m2, c, i2h, e); break;
+            case 5: vol_eval_canon<P, DIM, TC, PC(1, 0, 1)>(m0, m1, m2, c, i2h, e); break;
+            case 6: vol_eval_canon<P, DIM, TC, PC(1, 1, 0)>(m0, m1, m2, c, i2h, e); break;
+            default: vol_eval_canon<P, DIM, TC, PC(1, 1, 1)>(m0, m1, m2, c, i2h, e); break;
+        }
     }
 }
+
+// Phase-B order of the volume points: sorted by class, so the points a warp
+// evaluates together (32 / TC of them) share one evaluator where possible.
+template <int P, int DIM>
+struct VolOrder {
+    int p[27];
+};
+template <int P, int DIM>
+constexpr VolOrder<P, DIM> make_vol_order() {
+    VolOrder<P, DIM> o{};
+    constexpr int NQ = Shape<P, DIM>::NQ, NQZ = DIM == 3 ? NQ : 1, NVP = Shape<P, DIM>::NVP;
+    int n = 0;
+    for (int cls = 0; cls < 8; ++cls)
+        for (int q = 0; q < NVP; ++q) {
+            const int i = q / (NQ * NQZ), j = (q / NQZ) % NQ, k = q % NQZ;
+            const int c = (g_zero(NQ, i) ? 4 : 0) | (g_zero(NQ, j) ? 2 : 0) | (g_zero(NQZ, k) ? 1 : 0);
+            if (c == cls) o.p[n++] = q;
+        }
+    return o;
+}
+template <int P, int DIM>
+__device__ constexpr VolOrder<P, DIM> kVolOrder = make_vol_order<P, DIM>();
 
 // shared-memory plan of one cell-kernel CTA (doubles)
 template <int P, int DIM>
@@ -741,13 +719,13 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
 
         // ---- phase B: smooth fluxes at volume points
         for (int it = tid; it < TC * NVP; it += NT) {
-            const int l = it % TC, p = it / TC;
+            const int l = it % TC;
+            const int p = SH::NQ == 2 ? it / TC : kVolOrder<P, DIM>.p[it / TC];
             const int i = i0 + l;
             if (i >= nx) continue;
             const double i2h[3] = {gg[TC + l], i2hy, i2hz};
             double e[20];
-            if constexpr (SH::NQ == 2) vol_eval_sym<P, DIM, TC>(p, sc + l, i2h, e);
-            else vol_eval_rt<P, DIM, TC, NVP>(p, sc + l, i2h, e);
+            vol_eval_sym<P, DIM, TC>(p, sc + l, i2h, e);
             double o[30];
             double bad = 0.0;
             const int rc = smooth_flux<VISC, NAX>(e, kp.gas, o, bad);
