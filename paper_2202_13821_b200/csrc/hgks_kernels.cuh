@@ -728,14 +728,15 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
             vol_eval_sym<P, DIM, TC>(p, sc + l, i2h, e);
             double o[30];
             double bad = 0.0;
-            const int rc = smooth_flux<VISC, NAX>(e, kp.gas, o, bad);
+            const int rc = smooth_flux<VISC, NAX, MODE == MODE_STAGE2>(e, kp.gas, o, bad);
             if (rc) {
                 report_error(kp, err_key(kp.stage, 1, cglob_row + i, p, 0, rc), bad);
 #pragma unroll
                 for (int m = 0; m < 30; ++m) o[m] = 0.0;
             }
 #pragma unroll
-            for (int m = 0; m < 10 * NAX; ++m) vf[(p * 30 + m) * TC + l] = o[m];
+            for (int m = 0; m < 10 * NAX; ++m)
+                if (MODE != MODE_STAGE2 || m % 10 >= 5) vf[(p * 30 + m) * TC + l] = o[m];
         }
         if (kp.report) return;
         cp_async_wait<1>();  // this tile's face fluxes

@@ -528,7 +528,9 @@ HD int interface_flux(const double* tl, const double* tr, const GasC& g, const T
 // F_a = rho <u_a psi> - tau (rho sum_i <a_i u_i u_a psi> + FA_a), Ft_a = FA_a
 // (flux.hpp:128-165 + :180-189 in closed form). t = q[5], dq_x, dq_y, dq_z.
 // out[a][0..4] = F_a, out[a][5..9] = Ft_a.
-template <bool VISCOUS, int NAXES>
+// FT_ONLY (the S2O4 second stage, which uses only Lt): skip F, i.e. the
+// psi moments and the 9 viscous slope moments; out[a][5..9] only.
+template <bool VISCOUS, int NAXES, bool FT_ONLY = false>
 HD int smooth_flux(const double* t, const GasC& g, double* out, double& bad) {
     Prim w;
     const int rc = prim_from_q(t, g, w, bad);
@@ -544,6 +546,15 @@ HD int smooth_flux(const double* t, const GasC& g, double* out, double& bad) {
     double F0[5], FA[5], r[5], v[5];
 #pragma unroll
     for (int ax = 0; ax < NAXES; ++ax) {
+        if (FT_ONLY) {
+            if (ax == 0) slope_moment<1, 0, 0>(tb.U, tb, A, FA);
+            else if (ax == 1) slope_moment<0, 1, 0>(tb.U, tb, A, FA);
+            else slope_moment<0, 0, 1>(tb.U, tb, A, FA);
+            double* o = out + 10 * ax;
+#pragma unroll
+            for (int m = 0; m < 5; ++m) o[5 + m] = w.rho * FA[m];
+            continue;
+        }
         if (ax == 0) {
             psi_moment<1, 0, 0>(tb.U, tb, F0);
             slope_moment<1, 0, 0>(tb.U, tb, A, FA);
