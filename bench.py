@@ -298,11 +298,12 @@ def main():
         try:
             ex = json.load(open(exe_path))
             ef = ex["face_point"]["fp64_flops"] * ncell_local * nfp / (face_stage_ms * 1e-3) / 1e12
-            ec = ex["cell_stage"]["fp64_flops"] * ncell_local / (cell_stage_ms * 1e-3) / 1e12
+            cex = ex.get("cell_stage_mean", ex["cell_stage"])  # both S2O4 stages when captured
+            ec = cex["fp64_flops"] * ncell_local / (cell_stage_ms * 1e-3) / 1e12
             executed = {"face_tflops": ef, "face_frac": ef / peak if peak else None,
                         "cell_tflops": ec, "cell_frac": ec / peak if peak else None,
                         "face_fp64_inst_per_point": ex["face_point"]["dfma"] + ex["face_point"]["dmul"] + ex["face_point"]["dadd"],
-                        "cell_fp64_inst_per_cell_stage": ex["cell_stage"]["dfma"] + ex["cell_stage"]["dmul"] + ex["cell_stage"]["dadd"],
+                        "cell_fp64_inst_per_cell_stage": cex["dfma"] + cex["dmul"] + cex["dadd"],
                         "source": "profiles/executed_fp64_per_unit.json (ncu executed DFMA/DMUL/DADD per unit) / live CUDA-event time"}
         except Exception:  # noqa: BLE001
             executed = None
@@ -320,7 +321,7 @@ def main():
         ach = executed["face_tflops"] if dominant == "face" else executed["cell_tflops"]
         basis = ("executed FP64 flops per unit (2*DFMA + DMUL + DADD, ncu inst counts in "
                  "profiles/executed_fp64_per_unit.json): %.0f per face point, %.0f per cell-stage"
-                 % (ex["face_point"]["fp64_flops"], ex["cell_stage"]["fp64_flops"]))
+                 % (ex["face_point"]["fp64_flops"], ex.get("cell_stage_mean", ex["cell_stage"])["fp64_flops"]))
     else:
         ach = ach_face if dominant == "face" else ach_cell
         basis = ref_basis["flops_basis"]

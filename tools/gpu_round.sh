@@ -17,5 +17,7 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:face_kernel -s 6 -c 1 -o gpurun_out/prof_face -f $CMD > gpurun_out/ncu_face.log 2>&1; echo "rc=$?"
   echo "== ncu full cell"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:cell_kernel -s 2 -c 1 -o gpurun_out/prof_cell -f $CMD > gpurun_out/ncu_cell.log 2>&1; echo "rc=$?"
+  echo "== ncu full cell (stage 2)"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:cell_kernel -s 3 -c 1 -o gpurun_out/prof_cell2 -f $CMD > gpurun_out/ncu_cell2.log 2>&1; echo "rc=$?"
 fi
 lscpu | grep -E "Model name|^CPU\(s\)" > gpurun_out/host.txt

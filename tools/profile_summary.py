@@ -127,19 +127,30 @@ def main(tag):
         ncells = bench["config"]["cells"]
         nfp = {1: 4, 2: 4, 3: 9}[bench["config"]["degree"]]
         ex = {}
-        for name, units in (("face_point", ncells * nfp), ("cell_stage", ncells)):
-            t = fp64_per_launch(os.path.join(OUT, f"prof_{name.split('_')[0]}.ncu-rep"))
+        for name, rep, units in (("face_point", "prof_face", ncells * nfp), ("cell_stage", "prof_cell", ncells),
+                                 ("cell_stage2", "prof_cell2", ncells)):
+            path = os.path.join(OUT, f"{rep}.ncu-rep")
+            if not os.path.exists(path):
+                continue
+            t = fp64_per_launch(path)
             ex[name] = {k: v / units for k, v in t.items()}
             ex[name]["fp64_flops"] = 2 * ex[name]["dfma"] + ex[name]["dmul"] + ex[name]["dadd"]
-            ex[name]["kernel"] = traffic[name.split("_")[0]]["kernel"][:60]
+            ex[name]["kernel"] = raw(path)[0].get("Kernel Name", "")[:60]
+        if "cell_stage2" in ex:  # the two S2O4 stages differ (stage 2 computes only Lt)
+            ex["cell_stage_mean"] = {k: 0.5 * (ex["cell_stage"][k] + ex["cell_stage2"][k])
+                                     for k in ("dfma", "dmul", "dadd", "fp64_flops")}
         ex["source"] = f"ncu --set full source page, {tag}; units: face = cells*NFP points per launch, cell = cells"
         json.dump(ex, open(os.path.join(PROF, "executed_fp64_per_unit.json"), "w"), indent=1)
         md += ["## executed FP64 per unit", "",
                f"- face point: {ex['face_point']['dfma']:.0f} DFMA + {ex['face_point']['dmul']:.0f} DMUL + "
                f"{ex['face_point']['dadd']:.0f} DADD = {ex['face_point']['fp64_flops']:.0f} flops "
                f"(reference op count 8,503)",
-               f"- cell stage: {ex['cell_stage']['dfma']:.0f} DFMA + {ex['cell_stage']['dmul']:.0f} DMUL + "
-               f"{ex['cell_stage']['dadd']:.0f} DADD = {ex['cell_stage']['fp64_flops']:.0f} flops", ""]
+               f"- cell stage 1: {ex['cell_stage']['dfma']:.0f} DFMA + {ex['cell_stage']['dmul']:.0f} DMUL + "
+               f"{ex['cell_stage']['dadd']:.0f} DADD = {ex['cell_stage']['fp64_flops']:.0f} flops"]
+        if "cell_stage2" in ex:
+            md += [f"- cell stage 2: {ex['cell_stage2']['dfma']:.0f} DFMA + {ex['cell_stage2']['dmul']:.0f} DMUL + "
+                   f"{ex['cell_stage2']['dadd']:.0f} DADD = {ex['cell_stage2']['fp64_flops']:.0f} flops"]
+        md += [""]
     open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
     if "face" in traffic:
         t = traffic["face"]
