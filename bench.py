@@ -294,9 +294,13 @@ def main():
     # executed FP64 work per unit from the committed ncu capture (2 DFMA + DMUL + DADD)
     executed = None
     exe_path = os.path.join(ROOT, "profiles", "executed_fp64_per_unit.json")
-    if os.path.exists(exe_path) and a.degree == 2 and visc:
+    if os.path.exists(exe_path):
         try:
-            ex = json.load(open(exe_path))
+            ex_all = json.load(open(exe_path))
+            key = f"P{a.degree}_{'visc' if visc else 'inv'}"
+            ex = ex_all.get("families", {}).get(key) or (ex_all if key == "P2_visc" else None)
+            if ex is None:
+                raise KeyError(key)
             ef = ex["face_point"]["fp64_flops"] * ncell_local * nfp / (face_stage_ms * 1e-3) / 1e12
             cex = ex.get("cell_stage_mean", ex["cell_stage"])  # both S2O4 stages when captured
             ec = cex["fp64_flops"] * ncell_local / (cell_stage_ms * 1e-3) / 1e12
@@ -311,7 +315,7 @@ def main():
     # committed ncu capture) per CUDA-event second; the reference's op count
     # for the same unit (larger: the algebra here is restructured) is kept
     # beside it as 'reference_op_basis'
-    ref_basis = {
+    ref_basis = None if (a.degree, visc) not in F_CELL_RESIDUAL else {
         "flops_basis": "reference op count (SURVEY §8a/§8d): 8503 per face point, 162710 per cell-residual",
         "face": {"ms_per_stage": face_stage_ms, "tflops": ach_face, "frac": ach_face / peak if peak else None},
         "cell": {"ms_per_stage": cell_stage_ms, "tflops": ach_cell, "frac": ach_cell / peak if peak else None},
@@ -322,14 +326,16 @@ def main():
         basis = ("executed FP64 flops per unit (2*DFMA + DMUL + DADD, ncu inst counts in "
                  "profiles/executed_fp64_per_unit.json): %.0f per face point, %.0f per cell-stage"
                  % (ex["face_point"]["fp64_flops"], ex.get("cell_stage_mean", ex["cell_stage"])["fp64_flops"]))
-    else:
+    elif ref_basis is not None:
         ach = ach_face if dominant == "face" else ach_cell
         basis = ref_basis["flops_basis"]
+    else:  # P1 is an extension: the reference has no op count for it
+        ach, basis = None, "none (no executed capture for this family, no reference op count)"
     roof = {
         "bound": "fp64", "kernel": "face_kernel (3 launches = one face pass per stage)" if dominant == "face"
         else "cell_kernel (one launch per stage)",
         "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-        "frac": ach / peak if peak else None,
+        "frac": ach / peak if (peak and ach is not None) else None,
         "traffic": traffic,
         "peak_source": "live DFMA microbenchmark on this GPU (MEASURED_PEAKS.json has no FP64 entry)",
         "flops_basis": basis,

@@ -61,6 +61,41 @@ def fp64_per_launch(rep):
     return tot
 
 
+FAMILIES = {"P2_visc": ("tgv", 2, 128), "P1_visc": ("tgv", 1, 128), "P3_visc": ("tgv", 3, 64),
+            "P2_inv": ("adv3d", 2, 128), "P1_inv": ("adv3d", 1, 128), "P3_inv": ("adv3d", 3, 64)}
+
+
+def exec_family(key):
+    """Per-unit executed FP64 of one family from tools/exec_capture.sh's CSVs
+    (face: one axis pass = cells * NFP points; cell: stage 1 and stage 2)."""
+    case, deg, n = FAMILIES[key]
+    ncells = n ** 3
+    nfp = 9 if deg == 3 else 4
+    out = {}
+    for part, fname in (("face", f"exec_{key}_face.csv"), ("cell", f"exec_{key}_cell.csv")):
+        path = os.path.join(OUT, fname)
+        if not os.path.exists(path):
+            return None
+        rows = [r for r in csv.reader(open(path)) if len(r) > 14 and r[0].isdigit()]
+        per = defaultdict(dict)
+        for r in rows:
+            per[int(r[0])][r[12]] = num(r[14])
+            per[int(r[0])]["kernel"] = r[4]
+        for idx in sorted(per):
+            m = per[idx]
+            k = "face_point" if part == "face" else ("cell_stage" if ", 1>" in m["kernel"] else "cell_stage2")
+            units = ncells * nfp if part == "face" else ncells
+            e = {op: m.get(f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum", 0.0) / units
+                 for op in ("dfma", "dmul", "dadd")}
+            e["fp64_flops"] = 2 * e["dfma"] + e["dmul"] + e["dadd"]
+            e["kernel"] = m["kernel"][:60]
+            out[k] = e
+    if "cell_stage" in out and "cell_stage2" in out:
+        out["cell_stage_mean"] = {k: 0.5 * (out["cell_stage"][k] + out["cell_stage2"][k])
+                                  for k in ("dfma", "dmul", "dadd", "fp64_flops")}
+    return out
+
+
 def main(tag):
     os.makedirs(PROF, exist_ok=True)
     md = [f"# ncu summary {tag}", ""]
@@ -140,6 +175,11 @@ def main(tag):
             ex["cell_stage_mean"] = {k: 0.5 * (ex["cell_stage"][k] + ex["cell_stage2"][k])
                                      for k in ("dfma", "dmul", "dadd", "fp64_flops")}
         ex["source"] = f"ncu --set full source page, {tag}; units: face = cells*NFP points per launch, cell = cells"
+        fam = {k: v for k, v in ((k, exec_family(k)) for k in FAMILIES) if v}
+        if fam:
+            ex["families"] = fam
+            ex["families_source"] = ("tools/exec_capture.sh: ncu smsp__sass_thread_inst_executed_op_{dfma,dmul,dadd}"
+                                     "_pred_on.sum of one face launch and both cell stages per family")
         json.dump(ex, open(os.path.join(PROF, "executed_fp64_per_unit.json"), "w"), indent=1)
         md += ["## executed FP64 per unit", "",
                f"- face point: {ex['face_point']['dfma']:.0f} DFMA + {ex['face_point']['dmul']:.0f} DMUL + "
