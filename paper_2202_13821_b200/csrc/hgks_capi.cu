@@ -674,13 +674,14 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
     CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
     CK(cudaEventRecord(start, s->stream));  // after reset_error on the compute stream
     CK(cudaStreamWaitEvent(s->st_up, start, 0));
+    // the copy streams carry only copies (the AoS <-> SoA transposes run on
+    // the compute stream), so the copy engines never wait for an SM slot
+    // behind the persistent compute kernels
     for (int u = 0; u < N; ++u) {
         const int c = u == 0 ? N - 1 : u - 1;
         const long c0 = kb(c) * S, c1 = kb(c + 1) * S;
         CK(cudaMemcpyAsync(s->tmp + c0 * NC, q + c0 * NC, (size_t)(c1 - c0) * NC * sizeof(double),
                            cudaMemcpyHostToDevice, s->st_up));
-        aos_to_soa_kernel<<<tblocks, 256, 0, s->st_up>>>(kp0, s->tmp, s->qa, NC, c0, c1);
-        ++s->launches;
         CK(cudaEventRecord(s->ev_up[c], s->st_up));
     }
     cudaEventDestroy(start);
@@ -690,7 +691,18 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
     kp2.ft_only = 1;
     const KernelSet& K = s->ks;
     cudaStream_t cs = s->stream;
-    auto wait_up = [&](int c) { return cudaStreamWaitEvent(cs, s->ev_up[(c + N) % N], 0); };
+    // chunk c's upload landed -> transpose it into the SoA state (compute stream)
+    std::vector<char> landed(N, 0);
+    auto wait_up = [&](int c) {
+        c = (c + N) % N;
+        if (landed[c]) return cudaSuccess;
+        landed[c] = 1;
+        const cudaError_t e = cudaStreamWaitEvent(cs, s->ev_up[c], 0);
+        if (e != cudaSuccess) return e;
+        aos_to_soa_kernel<<<tblocks, 256, 0, cs>>>(kp0, s->tmp, s->qa, NC, kb(c) * S, kb(c + 1) * S);
+        ++s->launches;
+        return cudaGetLastError();
+    };
     auto F1 = [&](int c) { K.face_layers(kp1, s->qa, s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
     auto C1 = [&](int c) {
         K.cell_layers(kp1, MODE_STAGE1, s->qa, s->face, nullptr, nullptr, nullptr, s->qs, s->A, nullptr, cs,
@@ -701,7 +713,9 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
     auto C2 = [&](int c) {
         K.cell_layers(kp2, MODE_STAGE2, s->qs, s->face, nullptr, s->A, nullptr, s->qb, nullptr, nullptr, cs,
                       kb(c), kb(c + 1));
-        ++s->launches;
+        // q^{n+1} of chunk c -> AoS staging for its download
+        soa_to_aos_kernel<<<tblocks, 256, 0, cs>>>(kp0, s->qb, s->tmp2, NC, kb(c) * S, kb(c + 1) * S);
+        s->launches += 2;
         return cudaEventRecord(s->ev_c2[c], cs);
     };
     auto ghost = [&](double* a) {
@@ -731,8 +745,6 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
         const int c = d == N - 1 ? 0 : d + 1;
         const long c0 = kb(c) * S, c1 = kb(c + 1) * S;
         CK(cudaStreamWaitEvent(s->st_dn, s->ev_c2[c], 0));
-        soa_to_aos_kernel<<<tblocks, 256, 0, s->st_dn>>>(kp0, s->qb, s->tmp2, NC, c0, c1);
-        ++s->launches;
         CK(cudaMemcpyAsync(q + c0 * NC, s->tmp2 + c0 * NC, (size_t)(c1 - c0) * NC * sizeof(double),
                            cudaMemcpyDeviceToHost, s->st_dn));
     }
