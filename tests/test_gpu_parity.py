@@ -199,7 +199,8 @@ def test_tgv_diagnostics_match(hgks, oracle_mod):
     assert abs(rec.Ek - 0.125) <= 0.125 * 1e-3  # test_cases.cpp:140-150
 
 
-@pytest.mark.parametrize("case,n,degree,nchunks", [("tgv", 16, 2, 4), ("adv3d", 12, 2, 3), ("tgv", 8, 3, 4)])
+@pytest.mark.parametrize("case,n,degree,nchunks", [("tgv", 16, 2, 4), ("adv3d", 12, 2, 3), ("tgv", 8, 3, 4),
+                                                  ("tgv", 16, 2, 8), ("adv3d", 24, 2, 12), ("adv3d", 32, 1, 16)])
 def test_streamed_host_step_bitwise(hgks, case, n, degree, nchunks):
     """hgks_two_stage_step_host_streamed (chunked H2D / wavefront / D2H) gives
     the same bits as the serial host step and the device-resident step."""
