@@ -26,7 +26,8 @@ struct Launch {
     }
     // persistent face kernels: resident CTAs on the whole GPU per axis
     static inline int face_grid[3] = {0, 0, 0};
-    static int cell_smem() { return CellTile<P, DIM>::SMEM * (int)sizeof(double); }
+    template <int MODE = MODE_STAGE1>
+    static int cell_smem() { return CellTile<P, DIM, MODE>::SMEM * (int)sizeof(double); }
     // persistent cell kernel: resident CTAs on the whole GPU (set by configure)
     static inline int cell_grid[3] = {0, 0, 0};
 
@@ -82,12 +83,13 @@ struct Launch {
         const int first = ntx * kp.ny * kb, count = ntx * kp.ny * (ke - kb);
         if (count <= 0) return;
         const int grid = std::min(count, std::max(1, cell_grid[mode]));
-        const int smem = cell_smem();
         if (mode == MODE_STAGE1)
-            cell_kernel<P, DIM, VISC, MODE_STAGE1><<<grid, SH::NT_CELL, smem, st>>>(
+            cell_kernel<P, DIM, VISC, MODE_STAGE1><<<grid, CellTile<P, DIM, MODE_STAGE1>::NT,
+                                                     cell_smem<MODE_STAGE1>(), st>>>(
                 kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
         else
-            cell_kernel<P, DIM, VISC, MODE_STAGE2><<<grid, SH::NT_CELL, smem, st>>>(
+            cell_kernel<P, DIM, VISC, MODE_STAGE2><<<grid, CellTile<P, DIM, MODE_STAGE2>::NT,
+                                                     cell_smem<MODE_STAGE2>(), st>>>(
                 kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
     }
     static void face(const KParams& kp, const double* q, double* const f[3], cudaStream_t st,
@@ -109,15 +111,17 @@ struct Launch {
             count = 1;
             grid = 1;
         }
-        const int smem = cell_smem();
         if (mode == MODE_RESIDUAL)
-            cell_kernel<P, DIM, VISC, MODE_RESIDUAL><<<grid, SH::NT_CELL, smem, st>>>(
+            cell_kernel<P, DIM, VISC, MODE_RESIDUAL><<<grid, CellTile<P, DIM, MODE_RESIDUAL>::NT,
+                                                       cell_smem<MODE_RESIDUAL>(), st>>>(
                 kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
         else if (mode == MODE_STAGE1)
-            cell_kernel<P, DIM, VISC, MODE_STAGE1><<<grid, SH::NT_CELL, smem, st>>>(
+            cell_kernel<P, DIM, VISC, MODE_STAGE1><<<grid, CellTile<P, DIM, MODE_STAGE1>::NT,
+                                                     cell_smem<MODE_STAGE1>(), st>>>(
                 kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
         else
-            cell_kernel<P, DIM, VISC, MODE_STAGE2><<<grid, SH::NT_CELL, smem, st>>>(
+            cell_kernel<P, DIM, VISC, MODE_STAGE2><<<grid, CellTile<P, DIM, MODE_STAGE2>::NT,
+                                                     cell_smem<MODE_STAGE2>(), st>>>(
                 kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
     }
     static cudaError_t configure() {
@@ -129,9 +133,9 @@ struct Launch {
         set((const void*)face_kernel<P, DIM, VISC, 0>, face_smem<0>());
         set((const void*)face_kernel<P, DIM, VISC, 1>, face_smem<1>());
         set((const void*)face_kernel<P, DIM, VISC, 2>, face_smem<2>());
-        set((const void*)cell_kernel<P, DIM, VISC, MODE_RESIDUAL>, cell_smem());
-        set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE1>, cell_smem());
-        set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE2>, cell_smem());
+        set((const void*)cell_kernel<P, DIM, VISC, MODE_RESIDUAL>, cell_smem<MODE_RESIDUAL>());
+        set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE1>, cell_smem<MODE_STAGE1>());
+        set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE2>, cell_smem<MODE_STAGE2>());
         if (e != cudaSuccess) return e;
         int dev = 0, sms = 0;
         e = cudaGetDevice(&dev);
@@ -141,7 +145,10 @@ struct Launch {
                               (const void*)cell_kernel<P, DIM, VISC, MODE_STAGE2>};
         for (int m = 0; m < 3 && e == cudaSuccess; ++m) {
             int nb = 0;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fns[m], SH::NT_CELL, cell_smem());
+            const int nts[3] = {CellTile<P, DIM, MODE_RESIDUAL>::NT, CellTile<P, DIM, MODE_STAGE1>::NT,
+                                CellTile<P, DIM, MODE_STAGE2>::NT};
+            const int shm[3] = {cell_smem<MODE_RESIDUAL>(), cell_smem<MODE_STAGE1>(), cell_smem<MODE_STAGE2>()};
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fns[m], nts[m], shm[m]);
             cell_grid[m] = std::max(1, nb) * sms;
         }
         const void* ffn[3] = {(const void*)face_kernel<P, DIM, VISC, 0>,

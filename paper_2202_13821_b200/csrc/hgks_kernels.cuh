@@ -450,7 +450,6 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
 }
 
 // -------------------------------------------------------------- cell kernel
-enum : int { MODE_RESIDUAL = 0, MODE_STAGE1 = 1, MODE_STAGE2 = 2 };
 
 // value + global derivatives at a volume point of class PS (canonical index)
 // (eval_tabulated, dg.hpp:139-161); m0..m2: the point's sign masks
@@ -538,21 +537,32 @@ constexpr VolOrder<P, DIM> make_vol_order() {
 template <int P, int DIM>
 __device__ constexpr VolOrder<P, DIM> kVolOrder = make_vol_order<P, DIM>();
 
-// shared-memory plan of one cell-kernel CTA (doubles)
-template <int P, int DIM>
+enum : int { MODE_RESIDUAL = 0, MODE_STAGE1 = 1, MODE_STAGE2 = 2 };
+
+// shared-memory plan of one cell-kernel CTA (doubles). Face and volume flux
+// rows are (F|Ft) x var; the S2O4 second stage keeps only the Ft rows
+// (RW = 5, RO = 5), so its tile is half as large.
+template <int P, int DIM, int MODE>
 struct CellTile {
     using SH = Shape<P, DIM>;
     static constexpr int TC = SH::TC, NC = SH::NC, NVP = SH::NVP;
     static constexpr int NFX = SH::template nfp<0>(), NFY = SH::template nfp<1>(),
                          NFZ = SH::template nfp<2>();
+    static constexpr int RW = MODE == MODE_STAGE2 ? 5 : 10, RO = 10 - RW;
     static constexpr int COEF = NC * TC;           // one coefficient tile [NC][TC]
-    static constexpr int FX = NFX * 10 * (TC + 1); // x faces i0..i0+TC   [pf*10+c][TC+1]
-    static constexpr int FY = NFY * 10 * 2 * TC;   // y faces rows j, j+1 [pf*10+c][2][TC]
-    static constexpr int FZ = NFZ * 10 * 2 * TC;   // z faces layers k, k+1
-    static constexpr int VF = NVP * 30 * TC;       // volume-point fluxes [p][30][TC]
-    static constexpr int LB = 2 * NC * TC;         // L, Lt of the tile (stage-1 q*)
+    static constexpr int FX = NFX * RW * (TC + 1); // x faces i0..i0+TC   [pf*RW+c][TC+1]
+    static constexpr int FY = NFY * RW * 2 * TC;   // y faces rows j, j+1 [pf*RW+c][2][TC]
+    static constexpr int FZ = NFZ * RW * 2 * TC;   // z faces layers k, k+1
+    static constexpr int VFW = 3 * RW;             // flux rows per volume point
+    static constexpr int VF = NVP * VFW * TC;      // volume-point fluxes [p][VFW][TC]
+    static constexpr int LB = MODE == MODE_STAGE1 ? 2 * NC * TC : 0;  // L, Lt of the tile (stage-1 q*)
     static constexpr int GEO = 2 * TC + 4;          // widths of a tile: dx, 2/dx [TC]; dy, dz, 2/dy, 2/dz
     static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + LB + 2 * GEO;
+    // threads / resident CTAs: stage 2 (half the tile, ~150 registers) runs
+    // one thread per (cell, volume point) at 3 CTAs per SM for 3-D P1/P2
+    static constexpr bool S2X = MODE == MODE_STAGE2 && P < 3 && DIM == 3;
+    static constexpr int NT = S2X ? TC * NVP : SH::NT_CELL;
+    static constexpr int MINB = S2X ? 3 : SH::MINB_CELL;
 };
 
 // Persistent CTA over tiles of TC consecutive cells along x, software
@@ -563,7 +573,7 @@ struct CellTile {
 // projection + M^-1 (+ S2O4 combine); stage 1 then forms q* per coefficient
 // from shared memory, stage 2 needs only Lt2.
 template <int P, int DIM, bool VISC, int MODE>
-__global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CELL)
+__global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, MODE>::MINB)
     cell_kernel(KParams kp, const double* __restrict__ qin, const double* __restrict__ f0,
                 const double* __restrict__ f1, const double* __restrict__ f2,
                 const double* __restrict__ qn, const double* __restrict__ L1,
@@ -571,15 +581,15 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
                 double* __restrict__ out1, double* __restrict__ out2, int tile_first,
                 int tile_count, int unused) {
     using SH = Shape<P, DIM>;
-    using CT = CellTile<P, DIM>;
+    using CT = CellTile<P, DIM, MODE>;
     constexpr int N = SH::N, NC = SH::NC, NVP = SH::NVP, TC = SH::TC;
-    constexpr int NT = SH::NT_CELL, NAX = SH::NAX;
+    constexpr int NT = CT::NT, NAX = SH::NAX;
     extern __shared__ double smem[];
     double* coefb = smem;                 // [2][NC][TC]
     double* fx = coefb + 2 * CT::COEF;
     double* fy = fx + CT::FX;
     double* fz = fy + CT::FY;
-    double* vf = fz + CT::FZ;             // [NVP][30][TC]
+    double* vf = fz + CT::FZ;             // [NVP][VFW][TC]
     double* lb = vf + CT::VF;             // [2][NC][TC]
     double* geob = lb + CT::LB;           // [2][GEO], staged with the coefficients
 
@@ -633,7 +643,7 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
         }
     };
     // stage 2 consumes only the Ft rows (the face pass stores only those)
-    constexpr int RW = MODE == MODE_STAGE2 ? 5 : 10, RO = 10 - RW;
+    constexpr int RW = CT::RW, RO = CT::RO;
     auto face_row = [](int rr) { return (rr / RW) * 10 + RO + rr % RW; };
     auto prefetch_faces = [&](const TI& ti) {
         const int i0 = ti.i0, j = ti.j, k = ti.k;
@@ -664,13 +674,13 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
                 const double* sz = f2 + (long)r0 * kp.fs + oz;
 #pragma unroll
                 for (int pf = 0; pf < CT::NFX; ++pf)
-                    if (lane <= TC) cp_async8(fx + (pf * 10 + r0) * (TC + 1) + lane, sx + pf * pst, okx);
+                    if (lane <= TC) cp_async8(fx + (pf * RW + c) * (TC + 1) + lane, sx + pf * pst, okx);
 #pragma unroll
                 for (int pf = 0; pf < CT::NFY; ++pf)
-                    cp_async8(fy + (pf * 10 + r0) * 2 * TC + lane, sy + pf * pst, ok);
+                    cp_async8(fy + (pf * RW + c) * 2 * TC + lane, sy + pf * pst, ok);
 #pragma unroll
                 for (int pf = 0; pf < CT::NFZ; ++pf)
-                    cp_async8(fz + (pf * 10 + r0) * 2 * TC + lane, sz + pf * pst, ok);
+                    cp_async8(fz + (pf * RW + c) * 2 * TC + lane, sz + pf * pst, ok);
             }
         } else {
             for (int e = tid; e < CT::NFX * RW * (TC + 1); e += NT) {  // x faces i0 .. i0+TC (periodic wrap at nx)
@@ -678,19 +688,19 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
                 const int ig = i0 + l;
                 const bool ok = ig <= nx;  // x is always periodic: face nx is face 0
                 const int iw = ig == nx ? 0 : ig;
-                cp_async8(fx + r * (TC + 1) + l, f0 + (long)r * kp.fs + rowk + (ok ? iw : 0), ok);
+                cp_async8(fx + e, f0 + (long)r * kp.fs + rowk + (ok ? iw : 0), ok);
             }
             for (int e = tid; e < CT::NFY * RW * 2 * TC; e += NT) {  // y faces of rows j, j+1
                 const int l = e % (2 * TC), r = face_row(e / (2 * TC));
                 const int ig = i0 + (l % TC);
                 const bool ok = ig < nx;
-                cp_async8(fy + r * 2 * TC + l, f1 + (long)r * kp.fs + (l < TC ? rowk : rowp) + (ok ? ig : 0), ok);
+                cp_async8(fy + e, f1 + (long)r * kp.fs + (l < TC ? rowk : rowp) + (ok ? ig : 0), ok);
             }
             for (int e = tid; e < CT::NFZ * RW * 2 * TC; e += NT) {  // z faces of layers k, k+1
                 const int l = e % (2 * TC), r = face_row(e / (2 * TC));
                 const int ig = i0 + (l % TC);
                 const bool ok = ig < nx;
-                cp_async8(fz + r * 2 * TC + l, f2 + (long)r * kp.fs + (l < TC ? rowk : rowz) + (ok ? ig : 0), ok);
+                cp_async8(fz + e, f2 + (long)r * kp.fs + (l < TC ? rowk : rowz) + (ok ? ig : 0), ok);
             }
         }
     };
@@ -736,7 +746,7 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
             }
 #pragma unroll
             for (int m = 0; m < 10 * NAX; ++m)
-                if (MODE != MODE_STAGE2 || m % 10 >= 5) vf[(p * 30 + m) * TC + l] = o[m];
+                if (m % 10 >= RO) vf[(p * CT::VFW + (m / 10) * RW + m % 10 - RO) * TC + l] = o[m];
         }
         if (kp.report) return;
         cp_async_wait<1>();  // this tile's face fluxes
@@ -767,7 +777,7 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
                 for (int m = 0; m < N; ++m) acc[m] = 0.0;
 #pragma unroll
                 for (int pf = 0; pf < nfp; ++pf) {
-                    const int r = pf * 10 + row;
+                    const int r = pf * RW + row - RO;
                     double Fm, Fp;
                     if (a == 0) {
                         Fm = fx[r * (TC + 1) + l];
@@ -798,7 +808,7 @@ __global__ void __launch_bounds__(Shape<P, DIM>::NT_CELL, Shape<P, DIM>::MINB_CE
                 for (int m = 0; m < N; ++m) acc[m] = 0.0;
 #pragma unroll
                 for (int p = 0; p < NVP; ++p) {
-                    const double F = vf[(p * 30 + a * 10 + row) * TC + l];
+                    const double F = vf[(p * CT::VFW + a * RW + row - RO) * TC + l];
 #pragma unroll
                     for (int m = 0; m < N; ++m) {
                         const double c = ctab<P, DIM>.vw[p] * ctab<P, DIM>.vdB[p][a][m];
