@@ -59,19 +59,24 @@ HD int prim_from_q(const double* q, const GasC& g, Prim& w, double& bad) {
         bad = q[0];
         return ERR_DENSITY;
     }
-    const double inv = 1.0 / q[0];
-    const double p = g.gm1 * (q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) * inv);
-    if (!(p > 0.0)) {
-        bad = p;
+    // one reciprocal per state: with P = rho p = (gamma-1)(rho E - |m|^2/2)
+    // and r = 1/(rho P): 1/rho = P r, p/rho = P (1/rho)^2, lam = rho^3 r / 2
+    // (p > 0 <=> P > 0 for rho > 0; the division for the reported p is on
+    // the error path only)
+    const double P = g.gm1 * (q[4] * q[0] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]));
+    if (!(P > 0.0)) {
+        bad = P / q[0];
         return ERR_PRESSURE;
     }
+    const double r = 1.0 / (q[0] * P);
+    const double inv = P * r;
     w.rho = q[0];
     w.inv_rho = inv;
     w.U = q[1] * inv;
     w.V = q[2] * inv;
     w.W = q[3] * inv;
-    w.lam = 0.5 * q[0] / p;
-    w.il = p * inv;  // 1/(2 lam)
+    w.lam = 0.5 * (q[0] * q[0]) * (q[0] * r);
+    w.il = P * (inv * inv);  // p / rho = 1/(2 lam)
     return ERR_NONE;
 }
 
