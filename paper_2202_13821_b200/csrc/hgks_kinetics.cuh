@@ -80,6 +80,26 @@ HD int prim_from_q(const double* q, const GasC& g, Prim& w, double& bad) {
     return ERR_NONE;
 }
 
+// The same without an early exit: the state is formed unconditionally and
+// the checks become selects, so callers can keep one basic block (the
+// compiler then overlaps the division chain with independent work) and test
+// the code once at the end. Same codes and reported values as prim_from_q.
+HD int prim_from_q_nb(const double* q, const GasC& g, Prim& w, double& bad) {
+    const double P = g.gm1 * (q[4] * q[0] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]));
+    const double r = 1.0 / (q[0] * P);
+    const double inv = P * r;
+    w.rho = q[0];
+    w.inv_rho = inv;
+    w.U = q[1] * inv;
+    w.V = q[2] * inv;
+    w.W = q[3] * inv;
+    w.lam = 0.5 * (q[0] * q[0]) * (q[0] * r);
+    w.il = P * (inv * inv);
+    const bool okr = q[0] > 0.0, okp = P > 0.0;
+    bad = okr ? (P != 0.0 ? P * inv : 0.0) : q[0];
+    return okr ? (okp ? ERR_NONE : ERR_PRESSURE) : ERR_DENSITY;
+}
+
 // Per-state constants of the closed-form 5x5 micro-slope solve
 // (microslope.hpp:29-44).
 struct SolveC {
@@ -364,8 +384,7 @@ HD void directional_flux(const double* Ut, const T& t, const Slope* a, double* o
 template <bool VISCOUS, class Acc>
 HD int flux_side(const double* t, int side, const GasC& g, Acc& acc, double& p_side, double& bad) {
     Prim w;
-    const int rc = prim_from_q(t, g, w, bad);
-    if (rc) return rc;
+    const int rc = prim_from_q_nb(t, g, w, bad);  // checked at the end (one basic block)
     p_side = w.rho * w.il;
     const SolveC sc = solve_consts(w, g);
     // One table object: V, W full; U first full (for A), then overwritten by
@@ -409,7 +428,7 @@ HD int flux_side(const double* t, int side, const GasC& g, Acc& acc, double& p_s
 #pragma unroll
         for (int m = 0; m < 5; ++m) acc.nq(2, m) += w.rho * r[m];
     }
-    return ERR_NONE;
+    return rc;
 }
 
 // The merge split in two halves for two cooperating threads: both build the
@@ -425,8 +444,7 @@ struct MergeState {
 
 HD int merge_setup(const GasC& g, const double* q0, const double* dq0 /*[3][5]*/, MergeState& M,
                    double& bad) {
-    const int rc = prim_from_q(q0, g, M.w0, bad);
-    if (rc) return rc;
+    const int rc = prim_from_q_nb(q0, g, M.w0, bad);  // checked at the end
     M.s0 = solve_consts(M.w0, g);
     const double il = M.w0.il;
     full_seq<6>(M.w0.U, il, M.t0.U);
@@ -436,7 +454,7 @@ HD int merge_setup(const GasC& g, const double* q0, const double* dq0 /*[3][5]*/
     M.t0.dxi = 2.0 * g.K * il * il;
 #pragma unroll
     for (int d = 0; d < 3; ++d) M.ab[d] = micro_slope(M.s0, M.w0.inv_rho, dq0 + 5 * d);
-    return ERR_NONE;
+    return rc;
 }
 
 HD void merge_part_a(const MergeState& M, const TimeW& tw, double* F, double* Ft) {
@@ -486,8 +504,7 @@ HD int flux_merge(const GasC& g, const TimeW& tw, Acc& acc, double* F, double* F
         for (int d = 0; d < 3; ++d) dq0[5 * d + m] = acc.dq0(d, m);
     }
     MergeState M;
-    const int rc = merge_setup(g, q0, dq0, M, bad);
-    if (rc) return rc;
+    const int rc = merge_setup(g, q0, dq0, M, bad);  // checked at the end
     merge_part_a(M, tw, F, Ft);
     double Fb[5], Ftb[5];
     merge_part_b<VISCOUS>(M, tw, Fb, Ftb);
@@ -500,7 +517,7 @@ HD int flux_merge(const GasC& g, const TimeW& tw, Acc& acc, double* F, double* F
             Ft[m] += tw.f0Ft * acc.nq(0, m) + tw.anFt * acc.nq(1, m) + tw.AnFt * acc.nq(2, m);
         }
     }
-    return ERR_NONE;
+    return rc;
 }
 
 // Whole interface flux from two traces at a given tau; stage = 0 left,
@@ -538,8 +555,7 @@ HD int interface_flux(const double* tl, const double* tr, const GasC& g, const T
 template <bool VISCOUS, int NAXES, bool FT_ONLY = false>
 HD int smooth_flux(const double* t, const GasC& g, double* out, double& bad) {
     Prim w;
-    const int rc = prim_from_q(t, g, w, bad);
-    if (rc) return rc;
+    const int rc = prim_from_q_nb(t, g, w, bad);  // checked at the end
     const double tau = VISCOUS ? g.mu * (2.0 * w.lam * w.inv_rho) : 0.0;  // tau = mu/p (dg.hpp:433)
     const SolveC sc = solve_consts(w, g);
     Tab<6, 6> tb;
@@ -605,7 +621,7 @@ HD int smooth_flux(const double* t, const GasC& g, double* out, double& bad) {
             }
         }
     }
-    return ERR_NONE;
+    return rc;
 }
 
 }  // namespace hgks_dev
