@@ -291,17 +291,11 @@ struct TimeW {
 // rh = dt / (2 tau) and inv_dt = 1/dt are passed in so callers can form them
 // without a division (the face kernel has tau = 2 mu / (p_l + p_r))
 HD TimeW time_weights_r(double tau, double inv_dt, double rh) {
+    // branch-free: the general weights are formed and the tau = 0 limits
+    // (flux.hpp:32-38) selected, so the face point stays one basic block
     TimeW w;
-    if (!(tau > 0.0)) {  // tau = 0 branch (flux.hpp:32-38)
-        w.g0F = 1.0;
-        w.g0Ft = 0.0;
-        w.abF = w.abFt = 0.0;
-        w.AbF = 0.0;
-        w.AbFt = 1.0;
-        w.f0F = w.f0Ft = w.anF = w.anFt = w.AnF = w.AnFt = 0.0;
-        return w;
-    }
-    const double s = rh > 700.0 ? 1.0 : -expm1(-rh);  // 1 - e^{-dt/(2 tau)}, clamp flux.hpp:40
+    const double em = -expm1(-rh);
+    const double s = rh > 700.0 ? 1.0 : em;  // 1 - e^{-dt/(2 tau)}, clamp flux.hpp:40
     const double x = tau * inv_dt;
     const double t3 = s * (2.0 + s);
     const double ss = s * s;
@@ -319,6 +313,14 @@ HD TimeW time_weights_r(double tau, double inv_dt, double rh) {
     w.abFt = ab_t;
     w.anF = tau * (1.0 - ss) - 2.0 * tau * x * t3;
     w.anFt = -ab_t;
+    if (!(tau > 0.0)) {  // tau = 0 limits (flux.hpp:32-38), as selects
+        w.g0F = 1.0;
+        w.g0Ft = 0.0;
+        w.abF = w.abFt = 0.0;
+        w.AbF = 0.0;
+        w.AbFt = 1.0;
+        w.f0F = w.f0Ft = w.anF = w.anFt = w.AnF = w.AnFt = 0.0;
+    }
     return w;
 }
 
