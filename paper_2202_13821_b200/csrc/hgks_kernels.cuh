@@ -33,10 +33,10 @@
 #ifndef HGKS_FACE_STAGES
 #define HGKS_FACE_STAGES 2
 #endif
-// viscous P1/P2 face point as one basic block (both side passes + merge,
-// codes checked afterwards): 9.36 -> 8.85 ms per step; the inviscid flux
-// keeps the sequential passes (the single block costs it its 3 CTAs/SM), as
-// does P3 (measured 3% slower as one block)
+// P1/P2 face point as one basic block (both side passes + merge, codes
+// checked afterwards): TGV 9.36 -> 8.85 ms per step, adv3d 6.31 -> 6.04 (the
+// inviscid kernel still fits 3 CTAs/SM); P3 keeps the sequential passes
+// (measured 3% slower as one block)
 #ifndef HGKS_FACE_ONE_BLOCK
 #define HGKS_FACE_ONE_BLOCK 1
 #endif
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
             int fail = 0;
             double psum = 0.0;  // p_l + p_r of the traces
             double F[5], Ft[5];
-            if constexpr (VISC && P < 3 && HGKS_FACE_ONE_BLOCK) {
+            if constexpr (P < 3 && HGKS_FACE_ONE_BLOCK) {
             // both side passes and the merge without early exits: one basic
             // block, so the scheduler can overlap their dependency chains; the
             // codes are checked afterwards in the reference's order
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
                 fail = 1;
             }
             } else {
-            // inviscid (3 CTAs/SM at <= 168 registers): sequential passes
+            // P3: sequential passes
 #pragma unroll 1
             for (int side = 0; side < 2 && !fail; ++side) {
                 double tr[20];
