@@ -597,7 +597,9 @@ struct CellTile {
     static constexpr int VF = NVP * VFW * TC;      // volume-point fluxes [p][VFW][TC]
     static constexpr int LB = MODE == MODE_STAGE1 ? 2 * NC * TC : 0;  // L, Lt of the tile (stage-1 q*)
     static constexpr int GEO = 2 * TC + 4;          // widths of a tile: dx, 2/dx [TC]; dy, dz, 2/dy, 2/dz
-    static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + LB + 2 * GEO;
+    // stage 2: the tile's A = q + dt L1 + dt^2/6 Lt1 [NC][TC], prefetched with the faces
+    static constexpr int AB = MODE == MODE_STAGE2 ? COEF : 0;
+    static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + LB + 2 * GEO + AB;
     // threads / resident CTAs: stage 2 (half the tile, ~150 registers) runs
     // one thread per (cell, volume point) at 3 CTAs per SM for 3-D P1/P2
     static constexpr bool S2X = MODE == MODE_STAGE2 && P < 3 && DIM == 3;
@@ -632,6 +634,7 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
     double* vf = fz + CT::FZ;             // [NVP][VFW][TC]
     double* lb = vf + CT::VF;             // [2][NC][TC]
     double* geob = lb + CT::LB;           // [2][GEO], staged with the coefficients
+    double* ab = geob + 2 * CT::GEO;      // [NC][TC] stage 2: A of the tile
 
     const int tid = threadIdx.x;
     const int nx = kp.nx, ny = kp.ny;
@@ -650,8 +653,27 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
         r.j = a - r.k * ny;
         return r;
     };
-    auto prefetch_coef = [&](const TI& ti, double* dst, double* gdst) {
+    // one [NC][TC] state tile (coefficients of TC cells) -> shared memory
+    auto prefetch_state = [&](const double* __restrict__ base, const TI& ti, double* dst) {
         const long cbase = (long)(ti.k + 1) * kp.S + (long)ti.j * nx;
+        if constexpr (NT % TC == 0) {
+            // fixed column per thread, components strided by NT / TC
+            constexpr int CST = NT / TC;
+            const int l = tid % TC;
+            const bool ok = ti.i0 + l < nx;
+            const double* src = base + (long)(tid / TC) * kp.cs + cbase + (ok ? ti.i0 + l : 0);
+            const long sst = CST * kp.cs;
+#pragma unroll 4
+            for (int comp = tid / TC; comp < NC; comp += CST, src += sst) cp_async8(dst + comp * TC + l, src, ok);
+        } else {
+            for (int e = tid; e < CT::COEF; e += NT) {
+                const int l = e % TC, comp = e / TC;
+                const bool ok = ti.i0 + l < nx;
+                cp_async8(dst + comp * TC + l, base + comp * kp.cs + cbase + (ok ? ti.i0 + l : 0), ok);
+            }
+        }
+    };
+    auto prefetch_coef = [&](const TI& ti, double* dst, double* gdst) {
         // the tile's widths ride along (loaded through the async copy so their
         // latency is hidden like the coefficients')
         if (tid < TC) {
@@ -665,27 +687,13 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
                                                                                           : kp.i2dz + ti.k + 1;
             cp_async8(gdst + 2 * TC + r, src, true);
         }
-        if constexpr (NT % TC == 0) {
-            // fixed column per thread, components strided by NT / TC
-            constexpr int CST = NT / TC;
-            const int l = tid % TC;
-            const bool ok = ti.i0 + l < nx;
-            const double* src = qin + (long)(tid / TC) * kp.cs + cbase + (ok ? ti.i0 + l : 0);
-            const long sst = CST * kp.cs;
-#pragma unroll 4
-            for (int comp = tid / TC; comp < NC; comp += CST, src += sst) cp_async8(dst + comp * TC + l, src, ok);
-        } else {
-            for (int e = tid; e < CT::COEF; e += NT) {
-                const int l = e % TC, comp = e / TC;
-                const bool ok = ti.i0 + l < nx;
-                cp_async8(dst + comp * TC + l, qin + comp * kp.cs + cbase + (ok ? ti.i0 + l : 0), ok);
-            }
-        }
+        prefetch_state(qin, ti, dst);
     };
     // stage 2 consumes only the Ft rows (the face pass stores only those)
     constexpr int RW = CT::RW, RO = CT::RO;
     auto face_row = [](int rr) { return (rr / RW) * 10 + RO + rr % RW; };
     auto prefetch_faces = [&](const TI& ti) {
+        if (MODE == MODE_STAGE2) prefetch_state(L1, ti, ab);
         const int i0 = ti.i0, j = ti.j, k = ti.k;
         const long rowk = (long)nx * (j + (long)ny * k);
         const int jp = j + 1 == ny ? 0 : j + 1;
@@ -877,7 +885,7 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
                     } else {
                         // q^{n+1} = q + dt L1 + dt^2/6 (Lt1 + 2 Lt2) (integrator.hpp:72-74)
                         // = A + dt^2/6 * 2 Lt2, A formed by stage 1
-                        out0[gi] = __ldg(L1 + gi) + c6 * (2.0 * L);
+                        out0[gi] = ab[(m * 5 + v) * TC + l] + c6 * (2.0 * L);
                     }
                 }
             }
@@ -888,13 +896,17 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
             //   A  = q + (dt L1 + dt^2/6 Lt1)           -> out1 (stage 2 adds dt^2/6 * 2 Lt2)
             __syncthreads();
             const double c6 = dt * dt / 6.0;
+            // unrolled with predicated stores: all shared-memory loads of the
+            // thread's elements issue before the first use
+#pragma unroll
             for (int e = tid; e < NC * TC; e += NT) {
                 const int l = e % TC, comp = e / TC;
-                if (i0 + l >= nx) continue;
                 const double q = sc[comp * TC + l], L = lb[comp * TC + l], Lt = lb[(NC + comp) * TC + l];
                 const long gi = comp * kp.cs + cbase + i0 + l;
-                out0[gi] = q + 0.5 * dt * L + 0.125 * dt * dt * Lt;
-                out1[gi] = q + (dt * L + c6 * Lt);
+                if (i0 + l < nx) {
+                    out0[gi] = q + 0.5 * dt * L + 0.125 * dt * dt * Lt;
+                    out1[gi] = q + (dt * L + c6 * Lt);
+                }
             }
         }
         __syncthreads();  // buffers of this tile are free for the next prefetch
