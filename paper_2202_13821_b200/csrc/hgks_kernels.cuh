@@ -276,6 +276,43 @@ __device__ __forceinline__ void face_trace_sym(int p, const double* __restrict__
     }
 }
 
+// Tile walk of the persistent kernels: tile t = tx + ntx (j + ny k). The
+// stride (gridDim.x tiles) is decomposed once; each step is then a few adds
+// with carries instead of two integer divisions on the prefetch's critical path.
+struct TileWalk {
+    int ntx, ny, W;      // x tiles per row, rows, cells per x tile
+    int sx, sj, sk;      // stride in (tx, j, k)
+    __device__ __forceinline__ TileWalk(int ntx_, int ny_, int w, int step) : ntx(ntx_), ny(ny_), W(w) {
+        const int a = step / ntx;
+        sx = step - a * ntx;
+        sk = a / ny;
+        sj = a - sk * ny;
+    }
+    struct TI {
+        int i0, j, k, tx;
+    };
+    __device__ __forceinline__ TI of(int t) const {
+        const int a = t / ntx;
+        TI r;
+        r.tx = t - a * ntx;
+        r.i0 = r.tx * W;
+        r.k = a / ny;
+        r.j = a - r.k * ny;
+        return r;
+    }
+    __device__ __forceinline__ TI next(TI r) const {
+        r.tx += sx;
+        const int cx = r.tx >= ntx;
+        r.tx -= cx ? ntx : 0;
+        r.j += sj + cx;
+        const int cy = r.j >= ny;
+        r.j -= cy ? ny : 0;
+        r.k += sk + cy;
+        r.i0 = r.tx * W;
+        return r;
+    }
+};
+
 // async global->shared copies (cp.async, LDGSTS): the persistent kernels
 // prefetch the next tile while computing the current one
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
@@ -325,17 +362,8 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
     const int lane = tid & 31;
     const int warp = tid >> 5;
     // tile t -> (x offset, row j, layer k); computed once per tile
-    struct TI {
-        int i0, j, k;
-    };
-    auto tile_of = [&](int t) {
-        const int a = t / ntx;
-        TI r;
-        r.i0 = (t - a * ntx) * 32;
-        r.k = a / ny;
-        r.j = a - r.k * ny;
-        return r;
-    };
+    using TI = TileWalk::TI;
+    const TileWalk walk(ntx, ny, 32, step);
     // both neighbours' coefficients of one tile: lane = face, rows = components
     // (each warp streams its share of the 2*NC rows, 256 B per row)
     auto prefetch = [&](const TI& ti, double* dst) {
@@ -357,14 +385,14 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
     };
 
     const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
-    TI cur = tile_of(t0);
+    TI cur = walk.of(t0);
     if (t0 < tile_end) prefetch(cur, smem);
     cp_async_commit();
     int n = 0;
     for (int t = t0; t < tile_end; t += step, ++n) {
         double* sc = smem + (HGKS_FACE_STAGES == 2 ? (n & 1) * STG : 0);
         const bool has_next = t + step < tile_end;
-        const TI nxt = has_next ? tile_of(t + step) : cur;
+        const TI nxt = walk.next(cur);
         if (HGKS_FACE_STAGES == 2) {
             if (has_next) prefetch(nxt, smem + ((n + 1) & 1) * STG);
             cp_async_commit();
@@ -642,17 +670,8 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
     const int tile_end = tile_first + tile_count;
     const int step = kp.report ? tile_count : gridDim.x;
 
-    struct TI {
-        int i0, j, k;
-    };
-    auto tile_of = [&](int t) {
-        const int a = t / ntx;
-        TI r;
-        r.i0 = (t - a * ntx) * TC;
-        r.k = a / ny;
-        r.j = a - r.k * ny;
-        return r;
-    };
+    using TI = TileWalk::TI;
+    const TileWalk walk(ntx, ny, TC, step);
     // one [NC][TC] state tile (coefficients of TC cells) -> shared memory
     auto prefetch_state = [&](const double* __restrict__ base, const TI& ti, double* dst) {
         const long cbase = (long)(ti.k + 1) * kp.S + (long)ti.j * nx;
@@ -753,7 +772,7 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
         }
     };
     const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
-    TI cur = tile_of(t0);
+    TI cur = walk.of(t0);
     if (t0 < tile_end) prefetch_coef(cur, coefb, geob);
     cp_async_commit();
     const double dt = kp.dt;
@@ -763,7 +782,7 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
         prefetch_faces(cur);
         cp_async_commit();
         const bool has_next = t + step < tile_end;
-        const TI nxt = has_next ? tile_of(t + step) : cur;
+        const TI nxt = walk.next(cur);
         if (has_next) prefetch_coef(nxt, coefb + ((n + 1) & 1) * CT::COEF, geob + ((n + 1) & 1) * CT::GEO);
         cp_async_commit();
         const int i0 = cur.i0, j = cur.j, k = cur.k;
