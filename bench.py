@@ -309,6 +309,14 @@ def main():
                         "face_fp64_inst_per_point": ex["face_point"]["dfma"] + ex["face_point"]["dmul"] + ex["face_point"]["dadd"],
                         "cell_fp64_inst_per_cell_stage": cex["dfma"] + cex["dmul"] + cex["dadd"],
                         "source": "profiles/executed_fp64_per_unit.json (ncu executed DFMA/DMUL/DADD per unit) / live CUDA-event time"}
+            # FP64-pipe issue share: DMUL/DADD occupy the pipe like a DFMA but
+            # count one flop, so the flop fraction understates the pipe's load;
+            # the pipe issues peak/2 instructions per second (one DFMA = 2 flops)
+            if peak:
+                for k, n_units, ms in (("face", ncell_local * nfp, face_stage_ms),
+                                       ("cell", ncell_local, cell_stage_ms)):
+                    inst = executed[f"{k}_fp64_inst_per_point" if k == "face" else "cell_fp64_inst_per_cell_stage"]
+                    executed[f"{k}_pipe_frac"] = inst * n_units / (ms * 1e-3) / (peak * 1e12 / 2.0)
         except Exception:  # noqa: BLE001
             executed = None
     # headline: this kernel's own FP64 work (executed DFMA/DMUL/DADD from the
