@@ -144,6 +144,14 @@ HD Slope micro_slope(const SolveC& s, double inv_rho, const double* dq) {
                       inv_rho * dq[4]);
 }
 
+// rho * micro_slope: the solve is linear, so the flux passes carry slopes
+// pre-scaled by the state's density (a' = rho a) and drop both the 1/rho on
+// the way in and the rho on every slope-moment accumulation (the time
+// coefficient of a' slopes is rho A, also linear)
+HD Slope micro_slope_rho(const SolveC& s, const double* dq) {
+    return solve_unit(s, dq[0], dq[1], dq[2], dq[3], dq[4]);
+}
+
 // 1-D Gaussian moment recursion (moments.hpp:49-56)
 template <int NMAX>
 HD void full_seq(double us, double il, double* U) {
@@ -400,8 +408,8 @@ HD int flux_side(const double* t, int side, const GasC& g, Acc& acc, double& p_s
     tb.dxi = 2.0 * g.K * il * il;
     Slope a[3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) a[d] = micro_slope(sc, w.inv_rho, t + 5 + 5 * d);
-    Slope A{};
+    for (int d = 0; d < 3; ++d) a[d] = micro_slope_rho(sc, t + 5 + 5 * d);  // rho a
+    Slope A{};  // rho A
     if (VISCOUS) {
         // A from compatibility with the full table (flux.hpp:109-110)
         full_seq<5>(w.U, il, tb.U);
@@ -416,7 +424,7 @@ HD int flux_side(const double* t, int side, const GasC& g, Acc& acc, double& p_s
     for (int d = 0; d < 3; ++d) {
         slope_moment<0, 0, 0>(tb.U, tb, a[d], r);
 #pragma unroll
-        for (int m = 0; m < 5; ++m) acc.dq0(d, m) += w.rho * r[m];
+        for (int m = 0; m < 5; ++m) acc.dq0(d, m) += r[m];
     }
     if (VISCOUS) {
         // free-streaming moments of this side (flux.hpp:112-121), unweighted
@@ -425,10 +433,10 @@ HD int flux_side(const double* t, int side, const GasC& g, Acc& acc, double& p_s
         for (int m = 0; m < 5; ++m) acc.nq(0, m) += w.rho * r[m];
         directional_flux(tb.U, tb, a, r);
 #pragma unroll
-        for (int m = 0; m < 5; ++m) acc.nq(1, m) += w.rho * r[m];
+        for (int m = 0; m < 5; ++m) acc.nq(1, m) += r[m];
         slope_moment<1, 0, 0>(tb.U, tb, A, r);
 #pragma unroll
-        for (int m = 0; m < 5; ++m) acc.nq(2, m) += w.rho * r[m];
+        for (int m = 0; m < 5; ++m) acc.nq(2, m) += r[m];
     }
     return rc;
 }
@@ -441,7 +449,7 @@ struct MergeState {
     Prim w0;
     SolveC s0;
     Tab<6, 5> t0;
-    Slope ab[3];
+    Slope ab[3];  // rho0 abar
 };
 
 HD int merge_setup(const GasC& g, const double* q0, const double* dq0 /*[3][5]*/, MergeState& M,
@@ -455,12 +463,12 @@ HD int merge_setup(const GasC& g, const double* q0, const double* dq0 /*[3][5]*/
     M.t0.xi2 = g.K * il;
     M.t0.dxi = 2.0 * g.K * il * il;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) M.ab[d] = micro_slope(M.s0, M.w0.inv_rho, dq0 + 5 * d);
+    for (int d = 0; d < 3; ++d) M.ab[d] = micro_slope_rho(M.s0, dq0 + 5 * d);
     return rc;
 }
 
 HD void merge_part_a(const MergeState& M, const TimeW& tw, double* F, double* Ft) {
-    const Slope Ab = time_coefficient(M.s0, M.t0, M.ab);
+    const Slope Ab = time_coefficient(M.s0, M.t0, M.ab);  // rho0 Abar
     double r[5];
     psi_moment<1, 0, 0>(M.t0.U, M.t0, r);
     const double sF = M.w0.rho * tw.g0F, sFt = M.w0.rho * tw.g0Ft;
@@ -470,7 +478,7 @@ HD void merge_part_a(const MergeState& M, const TimeW& tw, double* F, double* Ft
         Ft[m] = sFt * r[m];
     }
     slope_moment<1, 0, 0>(M.t0.U, M.t0, Ab, r);
-    const double aF = M.w0.rho * tw.AbF, aFt = M.w0.rho * tw.AbFt;
+    const double aF = tw.AbF, aFt = tw.AbFt;
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
         F[m] += aF * r[m];
@@ -485,7 +493,7 @@ HD void merge_part_b(const MergeState& M, const TimeW& tw, double* F, double* Ft
     if (VISCOUS) {  // abar's weight vanishes at tau = 0 (flux.hpp:32-37)
         double r[5];
         directional_flux(M.t0.U, M.t0, M.ab, r);
-        const double sF = M.w0.rho * tw.abF, sFt = M.w0.rho * tw.abFt;
+        const double sF = tw.abF, sFt = tw.abFt;
 #pragma unroll
         for (int m = 0; m < 5; ++m) {
             F[m] = sF * r[m];
@@ -564,8 +572,8 @@ HD int smooth_flux(const double* t, const GasC& g, double* out, double& bad) {
     make_tab(w, g, tb);
     Slope a[3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) a[d] = micro_slope(sc, w.inv_rho, t + 5 + 5 * d);
-    const Slope A = time_coefficient(sc, tb, a);
+    for (int d = 0; d < 3; ++d) a[d] = micro_slope_rho(sc, t + 5 + 5 * d);  // rho a
+    const Slope A = time_coefficient(sc, tb, a);                                 // rho A
     double F0[5], FA[5], r[5], v[5];
 #pragma unroll
     for (int ax = 0; ax < NAXES; ++ax) {
@@ -575,7 +583,7 @@ HD int smooth_flux(const double* t, const GasC& g, double* out, double& bad) {
             else slope_moment<0, 0, 1>(tb.U, tb, A, FA);
             double* o = out + 10 * ax;
 #pragma unroll
-            for (int m = 0; m < 5; ++m) o[5 + m] = w.rho * FA[m];
+            for (int m = 0; m < 5; ++m) o[5 + m] = FA[m];
             continue;
         }
         if (ax == 0) {
@@ -611,15 +619,15 @@ HD int smooth_flux(const double* t, const GasC& g, double* out, double& bad) {
             }
 #pragma unroll
             for (int m = 0; m < 5; ++m) {
-                const double fvis = w.rho * (v[m] + r[m]) + w.rho * FA[m];
+                const double fvis = (v[m] + r[m]) + FA[m];
                 o[m] = w.rho * F0[m] - tau * fvis;
-                o[5 + m] = w.rho * FA[m];
+                o[5 + m] = FA[m];
             }
         } else {
 #pragma unroll
             for (int m = 0; m < 5; ++m) {
                 o[m] = w.rho * F0[m];
-                o[5 + m] = w.rho * FA[m];
+                o[5 + m] = FA[m];
             }
         }
     }
