@@ -103,7 +103,7 @@ HD int prim_from_q_nb(const double* q, const GasC& g, Prim& w, double& bad) {
 // Per-state constants of the closed-form 5x5 micro-slope solve
 // (microslope.hpp:29-44).
 struct SolveC {
-    double U, V, W, two_lam, c5f, qs;  // qs = q2 + sbar, c5f = 4 lam^2 / D
+    double U, V, W, two_lam, c5f2, hqs;  // hqs = (q2 + sbar)/2, c5f2 = 8 lam^2 / D
 };
 
 HD SolveC solve_consts(const Prim& w, const GasC& g) {
@@ -113,9 +113,9 @@ HD SolveC solve_consts(const Prim& w, const GasC& g) {
     s.W = w.W;
     const double q2 = w.U * w.U + w.V * w.V + w.W * w.W;
     const double sbar = g.D * w.il;  // 0.5 D / lam
-    s.qs = q2 + sbar;
+    s.hqs = 0.5 * (q2 + sbar);
     s.two_lam = 2.0 * w.lam;
-    s.c5f = (w.lam * w.lam) * g.four_D;  // 4 lam^2 / D
+    s.c5f2 = 2.0 * ((w.lam * w.lam) * g.four_D);  // 8 lam^2 / D
     return s;
 }
 
@@ -125,16 +125,18 @@ struct Slope {
 
 // solve <a psi> = r (r already divided by rho)
 HD Slope solve_unit(const SolveC& s, double r0, double r1, double r2, double r3, double r4) {
-    const double B = 2.0 * r4 - s.qs * r0;
+    // B/2 and the factor 2 moved into c5f2: power-of-two rescalings, so the
+    // same roundings as B = 2 r4 - qs r0, c5 = c5f (B - 2 (U R2 + V R3 + W R4))
+    const double hB = r4 - s.hqs * r0;
     const double R2 = r1 - s.U * r0;
     const double R3 = r2 - s.V * r0;
     const double R4 = r3 - s.W * r0;
     Slope a;
-    a.c5 = s.c5f * (B - 2.0 * (s.U * R2 + s.V * R3 + s.W * R4));
+    a.c5 = s.c5f2 * (hB - (s.U * R2 + s.V * R3 + s.W * R4));
     a.c2 = s.two_lam * R2 - s.U * a.c5;
     a.c3 = s.two_lam * R3 - s.V * a.c5;
     a.c4 = s.two_lam * R4 - s.W * a.c5;
-    a.c1 = r0 - s.U * a.c2 - s.V * a.c3 - s.W * a.c4 - 0.5 * a.c5 * s.qs;
+    a.c1 = r0 - s.U * a.c2 - s.V * a.c3 - s.W * a.c4 - a.c5 * s.hqs;
     return a;
 }
 
