@@ -259,13 +259,22 @@ HD void slope_moment(const double* Ut, const T& t, const Slope& a, double* r) {
 #define BE(q) (a.c3 * t.V[(q) + 1] + h5 * t.V[(q) + 2])
 #define GA(r) (a.c4 * t.W[(r) + 1] + h5 * t.W[(r) + 2])
 #define GG(p, q, r) ((t.V[q] * t.W[r]) * AL(p) + Ut[p] * (BE(q) * t.W[r] + t.V[q] * GA(r)))
-    const double g0 = GG(I, J, K);
+#define XT(q, r) (BE(q) * t.W[r] + t.V[q] * GA(r))
+    // G(I,J,K) and G(I+1,J,K) share the transverse part; in the energy
+    // moment the three second-order G's are regrouped by their common
+    // factors AL(I) and U_I (the V_q W_r sums depend on the table only)
+    const double vw = t.V[J] * t.W[K];
+    const double x0 = XT(J, K);
+    const double al0 = AL(I);
+    const double g0 = vw * al0 + Ut[I] * x0;
     r[0] = g0;
-    r[1] = GG(I + 1, J, K);
+    r[1] = vw * AL(I + 1) + Ut[I + 1] * x0;
     r[2] = GG(I, J + 1, K);
     r[3] = GG(I, J, K + 1);
-    r[4] = 0.5 * (GG(I + 2, J, K) + GG(I, J + 2, K) + GG(I, J, K + 2) + t.xi2 * g0 +
-                  (h5 * t.dxi) * (Ut[I] * (t.V[J] * t.W[K])));
+    r[4] = 0.5 * (vw * AL(I + 2) + Ut[I + 2] * x0 +
+                  al0 * (t.V[J + 2] * t.W[K] + t.V[J] * t.W[K + 2]) +
+                  Ut[I] * ((XT(J + 2, K) + XT(J, K + 2)) + (h5 * t.dxi) * vw) + t.xi2 * g0);
+#undef XT
 #undef AL
 #undef BE
 #undef GA
