@@ -103,7 +103,7 @@ HD int prim_from_q_nb(const double* q, const GasC& g, Prim& w, double& bad) {
 // Per-state constants of the closed-form 5x5 micro-slope solve
 // (microslope.hpp:29-44).
 struct SolveC {
-    double U, V, W, two_lam, c5f2, hqs;  // hqs = (q2 + sbar)/2, c5f2 = 8 lam^2 / D
+    double U, V, W, two_lam, c5f2, hqs, k1;  // hqs = (q2 + sbar)/2, c5f2 = 8 lam^2 / D, k1 = (q2 - sbar)/2
 };
 
 HD SolveC solve_consts(const Prim& w, const GasC& g) {
@@ -114,6 +114,7 @@ HD SolveC solve_consts(const Prim& w, const GasC& g) {
     const double q2 = w.U * w.U + w.V * w.V + w.W * w.W;
     const double sbar = g.D * w.il;  // 0.5 D / lam
     s.hqs = 0.5 * (q2 + sbar);
+    s.k1 = 0.5 * (q2 - sbar);
     s.two_lam = 2.0 * w.lam;
     s.c5f2 = 2.0 * ((w.lam * w.lam) * g.four_D);  // 8 lam^2 / D
     return s;
@@ -132,11 +133,14 @@ HD Slope solve_unit(const SolveC& s, double r0, double r1, double r2, double r3,
     const double R3 = r2 - s.V * r0;
     const double R4 = r3 - s.W * r0;
     Slope a;
-    a.c5 = s.c5f2 * (hB - (s.U * R2 + s.V * R3 + s.W * R4));
+    const double X = s.U * R2 + s.V * R3 + s.W * R4;
+    a.c5 = s.c5f2 * (hB - X);
     a.c2 = s.two_lam * R2 - s.U * a.c5;
     a.c3 = s.two_lam * R3 - s.V * a.c5;
     a.c4 = s.two_lam * R4 - s.W * a.c5;
-    a.c1 = r0 - s.U * a.c2 - s.V * a.c3 - s.W * a.c4 - a.c5 * s.hqs;
+    // r0 - U c2 - V c3 - W c4 - c5 qs/2 with c2..c4 substituted:
+    // r0 - 2 lam X + c5 (q2 - qs/2)
+    a.c1 = (r0 - s.two_lam * X) + a.c5 * s.k1;
     return a;
 }
 
