@@ -8,18 +8,25 @@ inverse mass + combine), the body of the reference's advance loop
 conserved-variable modal coefficient); a DOF-update = one DOF advanced one
 full step.
 
-* value   device-resident state, CUDA events on the solver stream, max over
-          ranks; the 839 MB state exceeds the 126 MB L2 (no flush needed).
+* value   device-resident state through the device advance loop
+          (hgks_advance_records: dt, clipping, commit and failure checks on
+          the GPU, one CUDA graph per step), CUDA events on the solver stream,
+          max over ranks; the 839 MB state exceeds the 126 MB L2 (no flush).
 * e2e     the same metric through the reference-facing C ABI call
-          hgks_two_stage_step_host(q_host, dt) on pinned host memory: H2D of
-          the state + step + D2H of the state inside the timed region.
+          hgks_two_stage_step_host_streamed(q_host, dt) on pinned host memory:
+          H2D of the state + step + D2H of the state inside the timed region.
 * roofline  dominant kernel (the face-flux pass) against the live-measured
-          DFMA peak of this GPU; algorithmic flops per face point = the
-          reference's own op count (8,503 with tau > 0).
-* cpu_baseline  the reference itself (oracle/_ref/libhgks_ref.so, headers
-          compiled unmodified) on this host's cores, bounded sample.
-Multi-GPU (torchrun): z-slabs, NCCL halo exchange of one coefficient layer per
-stage, dt min-allreduce; strong scaling (total 128^3 fixed).
+          DFMA peak of this GPU; achieved = the kernel's own EXECUTED FP64
+          flops (2 DFMA + DMUL + DADD per unit from the committed ncu capture,
+          profiles/executed_fp64_per_unit.json) / its CUDA-event time; the
+          reference's op count (8,503 per face point) is reported beside it.
+          roofline.hbm: per-kernel algorithmic GB/s and ncu DRAM bytes.
+* cpu_baseline  the reference itself (oracle/_ref, headers compiled
+          unmodified, -O3 -march=native when this CPU runs it) on this
+          host's cores, bounded sample.
+Multi-GPU (torchrun): z-slabs; the library's NCCL data plane moves one
+coefficient layer per stage and min-reduces dt and the error key on the
+device; strong scaling (total 128^3 fixed).
 """
 from __future__ import annotations
 
@@ -120,14 +127,32 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def host_cpu():
+    """CPU model and core count of this host (for the baseline's description)."""
+    model = "unknown CPU"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
 def cpu_reference_rate(a, budget, threads=None, warmup=1, steps=None):
-    """Time the reference (oracle/_ref) on the host: setup, warm-up, timed steps."""
+    """Time the reference (oracle/_ref) on the host: setup, warm-up, timed
+    steps. Prefers the build with the reference's own flags (-O3
+    -march=native, proj/CMakeLists.txt:13-16) when this CPU runs it."""
     import oracle as O
 
     if not O.ref_available():
         raise RuntimeError("oracle/_ref/libhgks_ref.so not built")
     threads = threads or os.cpu_count() or 1
-    r = O.RefRun(a.case, a.n, a.degree, workers=threads)
+    lib = "native" if O.native_ref_usable() else "portable"
+    flags = "-O3 -march=native (the reference's CMake flags)" if lib == "native" else \
+        "-O3 -march=x86-64-v3 (the -march=native build does not run on this CPU)"
+    r = O.RefRun(a.case, a.n, a.degree, workers=threads, lib=lib)
     cfl = a.cfl or (0.15 if a.degree == 2 else 0.09)
     dof = r.ncells * r.N * 5
     for _ in range(warmup):
@@ -139,7 +164,7 @@ def cpu_reference_rate(a, budget, threads=None, warmup=1, steps=None):
     for _ in range(n_steps):
         r.step(r.compute_dt(cfl))
     el = time.perf_counter() - t0
-    return dof * n_steps / el, threads, n_steps, el
+    return dof * n_steps / el, threads, n_steps, el, flags
 
 
 def run_reference_arm(a, rank, world):
@@ -147,7 +172,7 @@ def run_reference_arm(a, rank, world):
         return
     steps = max(1, min(a.steps, 3))
     try:
-        v, thr, n, el = cpu_reference_rate(a, a.cpu_budget, warmup=min(max(a.warmup, 0), 1), steps=steps)
+        v, thr, n, el, flags = cpu_reference_rate(a, a.cpu_budget, warmup=min(max(a.warmup, 0), 1), steps=steps)
     except Exception as e:  # noqa: BLE001
         print(json.dumps({"impl": "reference", "unavailable": f"reference CPU build failed: {e}"}))
         return
@@ -159,7 +184,8 @@ def run_reference_arm(a, rank, world):
         "config": {"workload": workload(a), "case": a.case, "n": a.n, "degree": a.degree},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": thr, "kind": "reference",
                          "sample": f"{a.case} P{a.degree} {a.n}^3, {n} full S2O4 steps after 1 warm-up "
-                                   f"(reference headers compiled unmodified, workers={thr})"},
+                                   f"(reference headers compiled unmodified, {flags}, workers={thr}, "
+                                   f"{host_cpu()[0]}, nproc {host_cpu()[1]})"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -206,6 +232,8 @@ def main():
     torch.cuda.set_stream(stream)
     s.set_stream(stream.cuda_stream)
     if world > 1:
+        # nccl: the library's own data plane (halo send/recv, dt and error-key
+        # reductions inside the per-step graph); gloo: the host-staged test mode
         slabs.attach(s, rank, world, local)
     visc = cfg.viscosity() > 0
     ncell_glob = r.mesh.ncells()
@@ -214,11 +242,12 @@ def main():
 
     peak = P.solver.measure_fp64_peak(local, 50.0) if rank == 0 else 0.0
 
-    # ---- warm-up, then K timed steps (compute_dt + S2O4 step each)
-    s.set_kernel_timing(True)
-    for _ in range(max(a.warmup, 0)):
-        s.step(s.compute_dt(cfl))
-    face_ms, cell_ms = [], []
+    # ---- warm-up, then K timed steps through the device-resident advance loop
+    # (compute_dt + S2O4 step each; dt, clipping, commit and failure checks on
+    # the device, one CUDA graph per step)
+    T_END = 1.0e9  # never reached: max_steps bounds the loop
+    for _ in range(1 if a.warmup > 0 else 0):
+        s.advance_records(T_END, cfl, 0.0, 0.0, 0.0, max_steps=max(a.warmup, 1))
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -226,15 +255,12 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
-        for _ in range(a.steps):
-            s.step(s.compute_dt(cfl))
-            f, c = s.kernel_times()
-            face_ms.append(f)
-            cell_ms.append(c)
+        steps_done = s.advance_records(T_END, cfl, 0.0, 0.0, 0.0, max_steps=a.steps)
         e1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    assert steps_done == a.steps, (steps_done, a.steps)
     launches = s.launch_count() - launches0
     el_ms = e0.elapsed_time(e1)
     t = torch.tensor([el_ms], dtype=torch.float64, device=coll_dev)
@@ -242,6 +268,17 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     el_ms = float(t.item())
     value = dof_glob * a.steps / (el_ms * 1e-3)
+
+    # ---- per-kernel split (outside the timed region): CUDA events around the
+    # face pass and the cell kernel of each stage, host-dt steps
+    s.set_kernel_timing(True)
+    face_ms, cell_ms = [], []
+    for _ in range(max(3, min(a.steps, 8))):
+        s.step(s.compute_dt(cfl))
+        f, c = s.kernel_times()
+        face_ms.append(f)
+        cell_ms.append(c)
+    s.set_kernel_timing(False)
 
     # ---- e2e through the C ABI with host buffers (rank-local state)
     e2e = None
@@ -283,13 +320,42 @@ def main():
     cell_stage_ms = statistics.median(cell_ms) / 2.0
     ach_face = f_face / (face_stage_ms * 1e-3) / 1e12
     ach_cell = f_cell / (cell_stage_ms * 1e-3) / 1e12
-    prof = os.path.join(ROOT, "profiles", "face_kernel_traffic.json")
-    traffic = None
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
-        except Exception:  # noqa: BLE001
-            traffic = None
+    # per-kernel HBM: algorithmic bytes per stage (the minimum each pass must
+    # move: face pass = the state read once per axis launch + its face-buffer
+    # writes; cell kernel = state + the three face buffers + its outputs) over
+    # the live event time; ncu-measured DRAM bytes of the same launches from
+    # the committed capture (profiles/kernel_traffic.json)
+    NC = s.N * 5
+    fpts = [s.face_points(ax) for ax in range(3)]
+    stage_bytes = {
+        "face": [sum(8.0 * ncell_local * (NC + fpts[ax] * 10) for ax in range(3)),
+                 sum(8.0 * ncell_local * (NC + fpts[ax] * 5) for ax in range(3))],
+        "cell": [8.0 * ncell_local * (NC + sum(fpts) * 10 + 2 * NC),
+                 8.0 * ncell_local * (NC + sum(fpts) * 5 + 2 * NC)],
+    }
+    hbm_peak = None
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm_peak = mp.get("hbm_gbs")
+    except Exception:  # noqa: BLE001
+        hbm_peak = None
+    hbm_src = "of measured (MEASURED_PEAKS.json hbm_gbs)" if hbm_peak else "of fallback (B200_PROFILING.md, 6.65 TB/s)"
+    hbm_peak = float(hbm_peak or 6650.0)
+    ncu_traffic = {}
+    try:
+        ncu_traffic = json.load(open(os.path.join(ROOT, "profiles", "kernel_traffic.json")))
+    except Exception:  # noqa: BLE001
+        ncu_traffic = {}
+    hbm = {}
+    for k, ms in (("face", face_stage_ms), ("cell", cell_stage_ms)):
+        byt = 0.5 * (stage_bytes[k][0] + stage_bytes[k][1])
+        gbs = byt / (ms * 1e-3) / 1e9
+        hbm[k] = {"algorithmic_bytes_per_stage": byt, "ms_per_stage": ms, "achieved_gbps": gbs,
+                  "frac_of_hbm": gbs / hbm_peak,
+                  "ncu_dram_bytes_per_stage": ncu_traffic.get(k, {}).get("dram_bytes_per_stage")}
+    hbm["peak_gbps"] = hbm_peak
+    hbm["peak_source"] = hbm_src
+    traffic = ncu_traffic.get("face", {}).get("dram_bytes_per_stage")
     dominant = "face" if face_stage_ms >= cell_stage_ms else "cell"
     # executed FP64 work per unit from the committed ncu capture (2 DFMA + DMUL + DADD)
     executed = None
@@ -345,7 +411,10 @@ def main():
         "achieved": ach, "peak": peak, "unit": "TFLOP/s",
         "frac": ach / peak if (peak and ach is not None) else None,
         "traffic": traffic,
+        "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum of the three face launches of one "
+                          "stage (profiles/kernel_traffic.json)",
         "peak_source": "live DFMA microbenchmark on this GPU (MEASURED_PEAKS.json has no FP64 entry)",
+        "hbm": hbm,
         "flops_basis": basis,
         "executed": executed,
         "reference_op_basis": ref_basis,
@@ -354,10 +423,11 @@ def main():
     cpu = None
     if not a.no_cpu_baseline and world == 1:
         try:
-            v, thr, n, el = cpu_reference_rate(a, a.cpu_budget, warmup=1)
+            v, thr, n, el, flags = cpu_reference_rate(a, a.cpu_budget, warmup=1)
             cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "reference",
                    "sample": f"{a.case} P{a.degree} {a.n}^3, {n} S2O4 step(s) after 1 warm-up, "
-                             f"{el:.1f} s, reference headers compiled unmodified, workers={thr}"}
+                             f"{el:.1f} s, reference headers compiled unmodified, {flags}, workers={thr}, "
+                             f"{host_cpu()[0]}, nproc {host_cpu()[1]}"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}

@@ -33,7 +33,7 @@ extern "C" {
 #define HGKS_ERR_DT 3
 #define HGKS_ERR_CUDA 4
 
-#define HGKS_ABI_VERSION 1
+#define HGKS_ABI_VERSION 2
 
 typedef struct hgks_solver hgks_solver;
 
@@ -97,14 +97,29 @@ int hgks_two_stage_step_host(hgks_solver* s, double* q, double dt);
 /* The same step with the host<->device traffic streamed: the z range is cut
  * into `nchunks` slabs whose uploads, face/cell kernels (a z-wavefront) and
  * downloads overlap on three streams. Results are bitwise identical to
- * hgks_two_stage_step_host. Difference: on a state error q may already hold
- * some advanced chunks (the device state is unchanged). Single slab only;
+ * hgks_two_stage_step_host; on a state error q is restored to q^n (the
+ * reference's two_stage_step leaves q untouched). Single slab only;
  * otherwise it falls back to hgks_two_stage_step_host. */
 int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int nchunks);
 
-/* advance() (solver.hpp:62-108) without records: steps from the current time
- * to t_end with dt = compute_dt (cfl) or dt_fixed (> 0), clipped to t_end and
- * to multiples of record_interval (> 0 only). Writes the number of steps taken. */
+/* advance() (solver.hpp:62-108), device-resident: steps from the current
+ * time to t_end with dt = compute_dt(cfl) or dt_fixed (> 0), clipped to t_end
+ * and, when record_interval > 0, to the next record time (the first one is
+ * first_record; the reference starts at record_interval). dt, the clipping,
+ * the t update and the failure checks run on the device (CUDA graph per
+ * step, no host round trip between steps); max_steps > 0 stops after that
+ * many steps. After every step that lands on a record time, on_record(user,
+ * s, t) is called with the solver showing that step's state (get_state,
+ * tgv_diagnostics, error_norms read it; the callback must not step s).
+ * State errors get " at t=<t>" appended (the failing step's start time);
+ * compute_dt failures are the bare error, as in the reference. On failure the
+ * state is q^n of the failing step. Writes the number of steps taken. */
+typedef int (*hgks_record_fn)(void* user, hgks_solver* s, double t);
+int hgks_advance_records(hgks_solver* s, double t_end, double cfl, double dt_fixed,
+                         double record_interval, double first_record, int max_steps,
+                         hgks_record_fn on_record, void* user, int* steps);
+/* the same without records: first_record = the next multiple of
+ * record_interval after the current time */
 int hgks_advance(hgks_solver* s, double t_end, double cfl, double dt_fixed,
                  double record_interval, int* steps);
 
@@ -160,9 +175,33 @@ void hgks_set_halo_exchange_split(hgks_solver* s, hgks_halo_fn start, hgks_halo_
  * stage 2 (needs q* ghosts), phase 2 = error check + commit. A single slab
  * fills its own ghosts; a multi-slab solver expects them unpacked already. */
 int hgks_step_phase(hgks_solver* s, double dt, int phase);
-/* dt reduction hook for multi-slab runs: min over ranks (order independent). */
-typedef int (*hgks_min_fn)(void* user, double* value);
-void hgks_set_dt_reduce(hgks_solver* s, hgks_min_fn fn, void* user);
+/* Host reduction hook for host-driven transports (halo callbacks): every
+ * rank calls it at the same points with op HGKS_REDUCE_MIN_U64 (error keys,
+ * dt bits: positive doubles order like their bits) or HGKS_REDUCE_SUM_F64
+ * (the offending value of a failure, diagnostics); the values are reduced in
+ * place over the slabs. Ranks whose own cells failed still join, so a state
+ * error raises the same, globally first, item on every rank. */
+#define HGKS_REDUCE_MIN_U64 0
+#define HGKS_REDUCE_SUM_F64 1
+typedef int (*hgks_reduce_fn)(void* user, int op, void* values, int n);
+void hgks_set_host_reduce(hgks_solver* s, hgks_reduce_fn fn, void* user);
+
+/* ---- in-library data plane: the z-slab ring over NCCL (NVLink / NVSwitch).
+ * Rank 0 creates an id (NCCL_UNIQUE_ID_BYTES = 128 bytes) and hands it to
+ * every rank (MPI_Bcast, torch.distributed, a file); each rank attaches its
+ * slab solver. The halo moves with ncclSend/ncclRecv on a comm stream while
+ * the ghost-free faces compute; dt and the error keys are min-reduced on the
+ * device (one 16-byte all-reduce per step for dt, 8 bytes for the key), so a
+ * step needs no host round trip. world = 1 runs the same exchange with the
+ * slab as its own neighbour. libnccl.so.2 is loaded at attach time
+ * (HGKS_NCCL_LIB overrides the name). */
+int hgks_nccl_unique_id(char* id_out, int nbytes);
+int hgks_attach_nccl(hgks_solver* s, const char* unique_id, int rank, int world);
+/* the same with a caller-owned communicator (an ncclComm_t) */
+int hgks_attach_nccl_comm(hgks_solver* s, void* nccl_comm, int rank, int world);
+/* in-place sum of n host doubles over the slabs (NCCL, or the host reduce
+ * hook; a single slab leaves them unchanged): diagnostics partial sums */
+int hgks_slab_reduce_sum(hgks_solver* s, double* values, int n);
 
 /* ---- runtime plumbing */
 int hgks_set_stream(hgks_solver* s, void* cuda_stream); /* NULL = solver-owned stream */
@@ -174,6 +213,12 @@ long hgks_launch_count(const hgks_solver* s);
  * the solver stream) when timing is enabled */
 void hgks_set_kernel_timing(hgks_solver* s, int on);
 int hgks_kernel_times(hgks_solver* s, double* face_ms, double* cell_ms, double* other_ms);
+/* CUDA graphs for the device-resident advance loop (default on; kernel
+ * timing disables them) */
+void hgks_set_graphs(hgks_solver* s, int on);
+/* test hook: cap the persistent face / cell grids at `ctas` CTAs (0 = the
+ * resident count), so every CTA walks many tiles even on small meshes */
+void hgks_set_grid_cap(hgks_solver* s, int ctas);
 
 /* Roofline denominator: sustained FP64 FMA throughput of `device`, measured
  * with a DFMA-chain kernel over ~`ms` milliseconds (CUDA events). Writes

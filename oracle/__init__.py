@@ -13,12 +13,18 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
+import sys
 
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libhgks_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libhgks_ref.so")
+# the reference built with its own CMake flags (-O3 -march=native), for the
+# CPU baseline; REF_SO (-march=x86-64-v3) is the portable checker
+REF_NATIVE_SO = os.path.join(HERE, "_ref", "libhgks_ref_native.so")
+# FMA contraction off: the C restatement's bitwise pin (tests/test_oracle.py)
+REF_NOFMA_SO = os.path.join(HERE, "_ref", "libhgks_ref_nofma.so")
 
 _dp = ctypes.POINTER(ctypes.c_double)
 
@@ -206,19 +212,32 @@ def orc_moments(prim, gamma):
 
 
 # --------------------------------------------------------------- reference
-_ref = None
+_ref = {}
 
 
 def ref_available() -> bool:
     return os.path.exists(REF_SO)
 
 
-def _ref_lib():
-    global _ref
-    if _ref is None:
-        if not os.path.exists(REF_SO):
-            raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference at build time)")
-        L = ctypes.CDLL(REF_SO)
+def native_ref_usable() -> bool:
+    """True if the -march=native reference build loads and steps on THIS
+    host's CPU (probed in a subprocess: an unsupported ISA would SIGILL)."""
+    if not os.path.exists(REF_NATIVE_SO):
+        return False
+    code = ("import sys; sys.path.insert(0, %r); import oracle as O; "
+            "r = O.RefRun('adv3d', 4, 2, lib='native'); r.step(r.compute_dt(0.15))" % os.path.dirname(HERE))
+    try:
+        return subprocess.run([sys.executable, "-c", code], capture_output=True, timeout=120).returncode == 0
+    except (OSError, subprocess.TimeoutExpired):
+        return False
+
+
+def _ref_lib(lib: str = "portable"):
+    if lib not in _ref:
+        path = {"native": REF_NATIVE_SO, "nofma": REF_NOFMA_SO}.get(lib, REF_SO)
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (needs /root/reference at build time)")
+        L = ctypes.CDLL(path)
         L.ref_setup.restype = ctypes.c_void_p
         L.ref_setup.argtypes = [ctypes.c_char_p] + [ctypes.c_int] * 4 + [ctypes.c_char_p, ctypes.c_int]
         L.ref_free.argtypes = [ctypes.c_void_p]
@@ -244,8 +263,8 @@ def _ref_lib():
                                       _dp, _dp, ctypes.c_char_p, ctypes.c_int]
         L.ref_maxwellian_moments.argtypes = [_dp, ctypes.c_double, _dp]
         L.ref_tables.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, _dp]
-        _ref = L
-    return _ref
+        _ref[lib] = L
+    return _ref[lib]
 
 
 class RefError(RuntimeError):
@@ -257,8 +276,8 @@ class RefError(RuntimeError):
 class RefRun:
     """The reference itself (setup_run + residual / step / advance)."""
 
-    def __init__(self, case, n, degree=2, nonuniform=False, workers=1):
-        L = _ref_lib()
+    def __init__(self, case, n, degree=2, nonuniform=False, workers=1, lib="portable"):
+        L = _ref_lib(lib)
         err = ctypes.create_string_buffer(512)
         self.h = L.ref_setup(case.encode(), n, degree, int(nonuniform), workers, err, 512)
         if not self.h:

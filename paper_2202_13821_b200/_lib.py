@@ -25,12 +25,17 @@ EXPORTS = [
     "hgks_abi_version", "hgks_create", "hgks_destroy", "hgks_last_error", "hgks_error_info",
     "hgks_num_basis", "hgks_num_coeffs", "hgks_face_points", "hgks_set_state", "hgks_get_state",
     "hgks_residual", "hgks_apply_inverse_mass", "hgks_compute_dt", "hgks_step",
-    "hgks_two_stage_step_host", "hgks_two_stage_step_host_streamed", "hgks_advance", "hgks_set_count_fluxes", "hgks_flux_evaluations",
+    "hgks_two_stage_step_host", "hgks_two_stage_step_host_streamed", "hgks_advance_records", "hgks_advance",
+    "hgks_set_count_fluxes", "hgks_flux_evaluations",
     "hgks_project_case", "hgks_tgv_diagnostics", "hgks_error_norms", "hgks_halo_bytes", "hgks_halo_buffers",
     "hgks_halo_pack", "hgks_halo_unpack", "hgks_set_halo_exchange", "hgks_set_halo_exchange_split", "hgks_step_phase",
-    "hgks_set_dt_reduce", "hgks_set_stream", "hgks_get_stream", "hgks_synchronize",
-    "hgks_launch_count", "hgks_set_kernel_timing", "hgks_kernel_times", "hgks_measure_fp64_peak",
+    "hgks_set_host_reduce", "hgks_nccl_unique_id", "hgks_attach_nccl", "hgks_attach_nccl_comm",
+    "hgks_slab_reduce_sum", "hgks_set_stream", "hgks_get_stream", "hgks_synchronize",
+    "hgks_launch_count", "hgks_set_kernel_timing", "hgks_kernel_times", "hgks_set_graphs", "hgks_set_grid_cap",
+    "hgks_measure_fp64_peak",
 ]
+
+HGKS_REDUCE_MIN_U64, HGKS_REDUCE_SUM_F64 = 0, 1
 
 
 class HgksConfig(ctypes.Structure):
@@ -44,7 +49,8 @@ class HgksConfig(ctypes.Structure):
 
 
 HALO_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int)
-MIN_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, _dp)
+REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int)
+RECORD_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double)
 
 _lib = None
 
@@ -81,6 +87,8 @@ def load():
     L.hgks_two_stage_step_host.argtypes = [sp, _dp, ctypes.c_double]
     L.hgks_two_stage_step_host_streamed.argtypes = [sp, _dp, ctypes.c_double, ctypes.c_int]
     L.hgks_advance.argtypes = [sp, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, _ip]
+    L.hgks_advance_records.argtypes = [sp, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_double, ctypes.c_int, RECORD_FN, sp, _ip]
     L.hgks_set_count_fluxes.argtypes = [sp, ctypes.c_int]
     L.hgks_set_count_fluxes.restype = None
     L.hgks_flux_evaluations.argtypes = [sp]
@@ -99,8 +107,16 @@ def load():
     L.hgks_set_halo_exchange.restype = None
     L.hgks_set_halo_exchange_split.argtypes = [sp, HALO_FN, HALO_FN, sp]
     L.hgks_set_halo_exchange_split.restype = None
-    L.hgks_set_dt_reduce.argtypes = [sp, MIN_FN, sp]
-    L.hgks_set_dt_reduce.restype = None
+    L.hgks_set_host_reduce.argtypes = [sp, REDUCE_FN, sp]
+    L.hgks_set_host_reduce.restype = None
+    L.hgks_nccl_unique_id.argtypes = [ctypes.c_char_p, ctypes.c_int]
+    L.hgks_attach_nccl.argtypes = [sp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]
+    L.hgks_attach_nccl_comm.argtypes = [sp, sp, ctypes.c_int, ctypes.c_int]
+    L.hgks_slab_reduce_sum.argtypes = [sp, _dp, ctypes.c_int]
+    L.hgks_set_graphs.argtypes = [sp, ctypes.c_int]
+    L.hgks_set_graphs.restype = None
+    L.hgks_set_grid_cap.argtypes = [sp, ctypes.c_int]
+    L.hgks_set_grid_cap.restype = None
     L.hgks_set_stream.argtypes = [sp, sp]
     L.hgks_get_stream.argtypes = [sp]
     L.hgks_get_stream.restype = sp

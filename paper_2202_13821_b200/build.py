@@ -77,7 +77,7 @@ def build(force: bool = False, verbose: bool = False, log: str | None = None) ->
             f.write(ptxas_log)
     if verbose:
         print(ptxas_log)
-    cmd = [nvcc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart"]
+    cmd = [nvcc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

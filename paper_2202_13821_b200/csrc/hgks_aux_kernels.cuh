@@ -111,6 +111,105 @@ __global__ void dt_kernel(KParams kp, const double* __restrict__ q, double cfl, 
     if ((threadIdx.x & 31) == 0) atomicMin(dt_bits, bits);
 }
 
+// ------------------------------------------------ step control on the device
+// Key block (unsigned 64-bit words, solver-owned): the two dt words are
+// min-reduced together across slabs (one 16-byte allreduce), the step key
+// after stage 2.
+enum : int { K_DTERR = 0, K_DT = 1, K_STEP = 2, K_FLUX = 3, K_SCRATCH = 4, K_WORDS = 8 };
+constexpr unsigned long long kNoKey = ~0ull;
+constexpr unsigned long long kInfBits = 0x7ff0000000000000ULL;
+
+// step scalars for a host-given dt (hgks_step, residual, streamed step)
+__global__ void set_scalars_kernel(double* scal, double dt, double mu) {
+    scal[SC_DT] = dt;
+    scal[SC_INV_DT] = dt != 0.0 ? 1.0 / dt : 0.0;
+    scal[SC_RH] = mu > 0.0 ? dt / (4.0 * mu) : 0.0;
+    scal[SC_ACTIVE] = 1.0;
+}
+
+// Control block of the device-resident advance loop (solver.hpp:90-107).
+struct StepCtl {
+    double t, t_end, next_record, record_interval, dt_fixed, mu;
+    unsigned long long fail_key;  // the key that halted the loop (step or dt)
+    int halted;                   // HALT_* below
+    int record;                   // clip dt to the record cadence
+    int steps;                    // committed steps
+    int rec_hit;                  // the last committed step landed on a record time
+};
+enum : int { HALT_NONE = 0, HALT_DONE = 1, HALT_STEP = 2, HALT_DT_STATE = 3, HALT_DT = 4 };
+// what the host reads back per step (pinned ring)
+struct StepStatus {
+    double t, dt;
+    unsigned long long fail_key;
+    int halted, steps, rec_hit, active;
+};
+
+// dt of the next step from the (reduced) dt words, clipped to t_end and the
+// next record time exactly as advance does (solver.hpp:90-93); a halted or
+// finished loop makes the step a no-op (SC_ACTIVE = 0).
+__global__ void dt_finalize_kernel(StepCtl* c, const unsigned long long* keys, double* scal) {
+    scal[SC_ACTIVE] = 0.0;
+    if (c->halted) return;
+    if (!(c->t < c->t_end - 1e-14 * c->t_end)) {
+        c->halted = HALT_DONE;
+        return;
+    }
+    double dt;
+    if (c->dt_fixed > 0.0) {
+        dt = c->dt_fixed;  // compute_dt's dt_fixed override (integrator.hpp:28)
+    } else {
+        if (keys[K_DTERR] != kNoKey) {
+            c->halted = HALT_DT_STATE;
+            c->fail_key = keys[K_DTERR];
+            return;
+        }
+        dt = __longlong_as_double((long long)keys[K_DT]);
+        if (!(dt > 0.0) || !isfinite(dt)) {  // integrator.hpp:43
+            c->halted = HALT_DT;
+            return;
+        }
+    }
+    const double rem = c->t_end - c->t;
+    dt = rem < dt ? rem : dt;  // std::min(dt, t_end - t)
+    if (c->record) {
+        const double rr = c->next_record - c->t;
+        dt = rr < dt ? rr : dt;
+    }
+    scal[SC_DT] = dt;
+    scal[SC_INV_DT] = 1.0 / dt;
+    scal[SC_RH] = c->mu > 0.0 ? dt / (4.0 * c->mu) : 0.0;
+    scal[SC_ACTIVE] = 1.0;
+}
+
+// After stage 2 (and the cross-slab key reduction): commit or halt, then
+// re-arm the dt words for the next step and publish the status.
+__global__ void commit_kernel(StepCtl* c, unsigned long long* keys, const double* scal, StepStatus* st) {
+    const bool active = scal[SC_ACTIVE] != 0.0;
+    if (active && !c->halted) {
+        if (keys[K_STEP] != kNoKey) {
+            c->halted = HALT_STEP;
+            c->fail_key = keys[K_STEP];
+        } else {
+            c->t += scal[SC_DT];  // t += dt (solver.hpp:101)
+            ++c->steps;
+            c->rec_hit = 0;
+            if (c->record && c->t >= c->next_record - 1e-12) {  // solver.hpp:104
+                c->rec_hit = 1;
+                c->next_record += c->record_interval;
+            }
+        }
+    }
+    keys[K_DT] = kInfBits;
+    keys[K_DTERR] = kNoKey;
+    st->t = c->t;
+    st->dt = active ? scal[SC_DT] : 0.0;
+    st->fail_key = c->fail_key;
+    st->halted = c->halted;
+    st->steps = c->steps;
+    st->rec_hit = active && !c->halted ? c->rec_hit : 0;
+    st->active = active ? 1 : 0;
+}
+
 // periodic single slab: ghost layer -1 <- layer nzl-1, ghost nzl <- layer 0
 __global__ void ghost_wrap_kernel(KParams kp, double* q, int ncomp) {
     const long per = (long)kp.S;

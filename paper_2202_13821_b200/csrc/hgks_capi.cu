@@ -1,13 +1,17 @@
 // C-ABI implementation of include/hgks_b200.h: the solver object, kernel
-// dispatch, host<->device layout transforms and the reference's error
-// semantics. There is no CPU path: every entry point that computes runs the
-// CUDA kernels of hgks_kernels.cuh and reports HGKS_ERR_CUDA if it cannot.
+// dispatch, host<->device layout transforms, the device-resident step loop
+// (dt, clipping, commit and error detection on the device, CUDA graphs), the
+// z-slab data plane over NCCL and the reference's error semantics. There is
+// no CPU path: every entry point that computes runs the CUDA kernels of
+// hgks_kernels.cuh / hgks_aux_kernels.cuh and reports HGKS_ERR_CUDA if it
+// cannot.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -16,6 +20,7 @@
 #include "hgks_aux_kernels.cuh"
 #include "hgks_kernels.cuh"
 #include "hgks_launch.h"
+#include "hgks_nccl.h"
 
 using namespace hgks_dev;
 
@@ -37,33 +42,55 @@ struct hgks_solver {
     KernelSet ks{};
     int N = 0, NC = 0;
     int nx = 0, ny = 0, nzl = 0, nz = 0, z0 = 0;
-    bool single = true;
+    bool single = true;  // one periodic slab: ghosts by the wrap kernel
     long S = 0, cs = 0, fs = 0;
     int zface_layers = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     // device memory
     double *d_tab = nullptr, *d_dx = nullptr, *d_dy = nullptr, *d_dz = nullptr;
-    // A = q^n + dt L1 + dt^2/6 Lt1: the only stage-1 residual output stage 2 needs
-    double *qa = nullptr, *qb = nullptr, *qs = nullptr, *A = nullptr;
+    // q^n = buf[cur]; a step writes q^{n+1} into buf[cur ^ 1] and the commit
+    // flips cur, so a failed step leaves q^n untouched
+    double* buf[2] = {nullptr, nullptr};
+    int cur = 0;
+    // q* and A = q^n + dt L1 + dt^2/6 Lt1 (the only stage-1 output stage 2 needs)
+    double *qs = nullptr, *A = nullptr;
     double *R = nullptr, *Rt = nullptr, *tmp = nullptr, *tmp2 = nullptr;
     // streamed host step: copy streams and per-chunk events
     cudaStream_t st_up = nullptr, st_dn = nullptr;
     std::vector<cudaEvent_t> ev_up, ev_c2, ev_dn;
     double* face[3] = {nullptr, nullptr, nullptr};
-    unsigned long long* d_key = nullptr;  // [0] error key, [1] dt bits, [2] flux count
-    double* d_val = nullptr;
-    double* d_red = nullptr;  // reduction scratch
+    unsigned long long* d_key = nullptr;  // K_* words (hgks_aux_kernels.cuh)
+    double* d_val = nullptr;              // report value of a failure
+    double* d_red = nullptr;              // reduction scratch
+    double* d_scal = nullptr;             // [2][SC_SLOT] step scalars (slot = step parity)
+    StepCtl* d_ctl = nullptr;             // device-resident advance loop
+    StepStatus* d_stat = nullptr;
+    StepStatus* h_stat = nullptr;         // pinned [2]
+    cudaEvent_t ev_stat[2] = {nullptr, nullptr};
     double time = 0.0;
-    // hooks
+    // host-driven transports (torch.distributed callbacks; CPU tests / gloo)
     hgks_halo_fn halo = nullptr;
     void* halo_user = nullptr;
     hgks_halo_fn halo_start = nullptr, halo_finish = nullptr;  // overlapped exchange
     void* halo_split_user = nullptr;
-    hgks_min_fn dtmin = nullptr;
-    void* dtmin_user = nullptr;
-    double* d_halo = nullptr;  // [4][NC][S]: send_lo, send_hi, recv_lo, recv_hi
+    hgks_reduce_fn hreduce = nullptr;
+    void* hreduce_user = nullptr;
+    double* d_halo = nullptr;    // [4][NC][S]: send_lo, send_hi, recv_lo, recv_hi
     bool external_halo = false;  // hgks_step_phase: caller exchanges ghosts
+    // in-library data plane: NCCL communicator over the z-slab ring
+    ncclComm_t comm = nullptr;
+    bool own_comm = false;
+    int rank = 0, world = 1;
+    cudaStream_t st_comm = nullptr;
+    cudaEvent_t ev_pack = nullptr, ev_xfer = nullptr;
+    // captured device steps (one per buffer parity), valid for (cfl, fixed)
+    bool use_graphs = true;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    long glaunches[2] = {0, 0};
+    double g_cfl = -1.0;
+    int g_fixed = -1;
+    int grid_cap = 0;
     bool count_fluxes = false;
     long flux_evals = 0;
     long launches = 0;
@@ -75,6 +102,11 @@ struct hgks_solver {
     int e_code = 0, e_phase = -1;
     long e_item = -1;
     double e_value = 0.0;
+
+    double* qa() const { return buf[cur]; }
+    double* qb() const { return buf[cur ^ 1]; }
+    bool nccl_on() const { return comm != nullptr; }
+    bool host_hooks() const { return !single && !nccl_on() && !external_halo; }
 };
 
 namespace {
@@ -91,13 +123,37 @@ int cuda_fail(hgks_solver* s, cudaError_t e, const char* where) {
     return fail(s, HGKS_ERR_CUDA, std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e));
 }
 
+// Scoped device guard: every entry point that touches device memory or a
+// stream runs on the solver's device and restores the caller's current device.
+struct DevGuard {
+    int prev = -1, want;
+    explicit DevGuard(int d) : want(d) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != want) cudaSetDevice(want);
+    }
+    ~DevGuard() {
+        if (prev >= 0 && prev != want) cudaSetDevice(prev);
+    }
+};
+#define GUARD(s) DevGuard _dev_guard((s) ? (s)->cfg.device : 0)
+
 #define CK(call)                                                   \
     do {                                                           \
         cudaError_t _e = (call);                                   \
         if (_e != cudaSuccess) return cuda_fail(s, _e, #call);     \
     } while (0)
 
-KParams make_params(hgks_solver* s, double dt, int stage) {
+#define NK(call)                                                                              \
+    do {                                                                                      \
+        ncclResult_t _r = (call);                                                             \
+        if (_r != ncclSuccess)                                                                \
+            return fail(s, HGKS_ERR_CUDA, std::string("NCCL error in ") + #call + ": " +      \
+                                              nccl().GetErrorString(_r));                     \
+    } while (0)
+
+double* scal_slot(hgks_solver* s, int slot) { return s->d_scal + slot * SC_SLOT; }
+
+KParams make_params(hgks_solver* s, int stage, int slot) {
     KParams kp{};
     kp.nx = s->nx;
     kp.ny = s->ny;
@@ -113,10 +169,9 @@ KParams make_params(hgks_solver* s, double dt, int stage) {
     kp.count_fluxes = s->count_fluxes ? 1 : 0;
     kp.report = 0;
     kp.ft_only = 0;
-    kp.dt = dt;
-    kp.inv_dt = dt != 0.0 ? 1.0 / dt : 0.0;
+    kp.scal = scal_slot(s, slot);
     kp.two_mu = 2.0 * s->cfg.mu;
-    kp.rh_coef = s->cfg.mu > 0.0 ? dt / (4.0 * s->cfg.mu) : 0.0;
+    kp.grid_cap = s->grid_cap;
     kp.gas.gamma = s->cfg.gamma;
     kp.gas.gm1 = s->cfg.gamma - 1.0;
     kp.gas.K = (5.0 - 3.0 * s->cfg.gamma) / (s->cfg.gamma - 1.0);
@@ -146,9 +201,9 @@ KParams make_params(hgks_solver* s, double dt, int stage) {
     kp.off_pw = t.off_pw;
     kp.off_pref = t.off_pref;
     kp.off_massf = t.off_massf;
-    kp.err_key = s->d_key;
+    kp.err_key = s->d_key + K_STEP;
     kp.err_val = s->d_val;
-    kp.flux_count = s->d_key + 2;
+    kp.flux_count = s->d_key + K_FLUX;
     return kp;
 }
 
@@ -158,92 +213,222 @@ std::string fmt_f(double v) {  // std::to_string(double) == "%f"
     return b;
 }
 
-double* which_array(hgks_solver* s, int which) { return which == 0 ? s->qa : s->qs; }
+void drop_graphs(hgks_solver* s) {
+    for (auto& g : s->gexec)
+        if (g) {
+            cudaGraphExecDestroy(g);
+            g = nullptr;
+        }
+    s->g_cfl = -1.0;
+    s->g_fixed = -1;
+}
 
-int halo_pack(hgks_solver* s, int which) {
-    KParams kp = make_params(s, 0.0, 0);
-    const long total = s->S * s->NC;
-    const int blocks = (int)std::min<long>((total + 255) / 256, 148L * 16);
-    halo_pack_kernel<<<blocks, 256, 0, s->stream>>>(kp, which_array(s, which), s->d_halo, s->NC);
+int set_scalars(hgks_solver* s, int slot, double dt) {
+    set_scalars_kernel<<<1, 1, 0, s->stream>>>(scal_slot(s, slot), dt, s->cfg.mu);
     ++s->launches;
     CK(cudaGetLastError());
     return HGKS_OK;
 }
 
-int halo_unpack(hgks_solver* s, int which) {
-    KParams kp = make_params(s, 0.0, 0);
+int halo_pack(hgks_solver* s, const double* a) {
+    KParams kp = make_params(s, 0, 0);
     const long total = s->S * s->NC;
     const int blocks = (int)std::min<long>((total + 255) / 256, 148L * 16);
-    halo_unpack_kernel<<<blocks, 256, 0, s->stream>>>(kp, which_array(s, which), s->d_halo, s->NC);
+    halo_pack_kernel<<<blocks, 256, 0, s->stream>>>(kp, a, s->d_halo, s->NC);
     ++s->launches;
     CK(cudaGetLastError());
     return HGKS_OK;
 }
 
-// fill ghost layers of array `which` before a residual: periodic wrap for a
-// single slab; pack -> user exchange -> unpack for a slab of a multi-slab run
-// (skipped when the caller drives the exchange through hgks_step_phase)
-int fill_ghosts(hgks_solver* s, int which) {
+int halo_unpack(hgks_solver* s, double* a) {
+    KParams kp = make_params(s, 0, 0);
+    const long total = s->S * s->NC;
+    const int blocks = (int)std::min<long>((total + 255) / 256, 148L * 16);
+    halo_unpack_kernel<<<blocks, 256, 0, s->stream>>>(kp, a, s->d_halo, s->NC);
+    ++s->launches;
+    CK(cudaGetLastError());
+    return HGKS_OK;
+}
+
+// NCCL halo: send_lo -> lower neighbour's recv_hi, send_hi -> upper's recv_lo
+// (fixed posting order, so world 1 (self) and world 2 (both neighbours the
+// same peer) match too), on the comm stream behind the pack.
+int nccl_exchange_start(hgks_solver* s) {
+    const NcclApi& N = nccl();
+    const size_t L = (size_t)s->S * s->NC;
+    const int lo = (s->rank - 1 + s->world) % s->world, hi = (s->rank + 1) % s->world;
+    CK(cudaEventRecord(s->ev_pack, s->stream));
+    CK(cudaStreamWaitEvent(s->st_comm, s->ev_pack, 0));
+    NK(N.GroupStart());
+    NK(N.Send(s->d_halo, L, ncclDouble, lo, s->comm, s->st_comm));
+    NK(N.Recv(s->d_halo + 3 * L, L, ncclDouble, hi, s->comm, s->st_comm));
+    NK(N.Send(s->d_halo + L, L, ncclDouble, hi, s->comm, s->st_comm));
+    NK(N.Recv(s->d_halo + 2 * L, L, ncclDouble, lo, s->comm, s->st_comm));
+    NK(N.GroupEnd());
+    CK(cudaEventRecord(s->ev_xfer, s->st_comm));
+    return HGKS_OK;
+}
+
+int nccl_exchange_finish(hgks_solver* s) {
+    CK(cudaStreamWaitEvent(s->stream, s->ev_xfer, 0));
+    return HGKS_OK;
+}
+
+// in-place min (u64) / sum (f64) over the slab ring, on the solver stream
+int nccl_reduce(hgks_solver* s, void* dev, int n, bool u64_min) {
+    NK(nccl().AllReduce(dev, dev, (size_t)n, u64_min ? ncclUint64 : ncclDouble, u64_min ? ncclMin : ncclSum,
+                        s->comm, s->stream));
+    return HGKS_OK;
+}
+
+// fill ghost layers of `a` (no-overlap transports)
+int fill_ghosts(hgks_solver* s, double* a) {
     if (s->single) {
-        KParams kp = make_params(s, 0.0, 0);
+        KParams kp = make_params(s, 0, 0);
         const long total = s->S * s->NC * 2;
         const int blocks = (int)std::min<long>((total + 255) / 256, 148L * 16);
-        ghost_wrap_kernel<<<blocks, 256, 0, s->stream>>>(kp, which_array(s, which), s->NC);
+        ghost_wrap_kernel<<<blocks, 256, 0, s->stream>>>(kp, a, s->NC);
         ++s->launches;
         CK(cudaGetLastError());
         return HGKS_OK;
     }
     if (s->external_halo) return HGKS_OK;
     if (!s->halo) return fail(s, HGKS_ERR_CONFIG, "multi-slab solver has no halo exchange set");
-    int rc = halo_pack(s, which);
+    const int which = a == s->qs ? 1 : 0;
+    int rc = halo_pack(s, a);
     if (rc) return rc;
     if (s->halo(s->halo_user, s, which) != 0) return fail(s, HGKS_ERR_CUDA, "halo exchange callback failed");
-    return halo_unpack(s, which);
+    return halo_unpack(s, a);
 }
 
-int reset_error(hgks_solver* s) {
-    const unsigned long long init[2] = {~0ull, ~0ull};
+int reset_keys(hgks_solver* s) {
+    static const unsigned long long init[3] = {kNoKey, kInfBits, kNoKey};  // K_DTERR, K_DT, K_STEP
     CK(cudaMemcpyAsync(s->d_key, init, sizeof init, cudaMemcpyHostToDevice, s->stream));
     return HGKS_OK;
 }
 
-// Decode the winning error key; re-run the failing tile in report mode to get
-// the offending value; shape the message as the reference does.
-int finish_error(hgks_solver* s, unsigned long long key, const double* stage_inputs[2],
-                 double dt) {
+void ev_record(hgks_solver* s, int i) {
+    if (s->timing) cudaEventRecord(s->ev[i], s->stream);
+}
+
+// One residual evaluation of `in` (ghosts filled here) in the given mode,
+// with the step scalars of `slot`.
+int run_residual(hgks_solver* s, double* in, int stage, int slot, int mode, double* o0, double* o1) {
+    KParams kp = make_params(s, stage, slot);
+    kp.ft_only = mode == MODE_STAGE2;
+    const bool split_cb = s->host_hooks() && s->halo_start;
+    if (!s->single && !s->external_halo && (s->nccl_on() || split_cb)) {
+        // overlapped halo: pack -> start the exchange -> faces that need no
+        // ghost (x, y faces of every owned layer, z faces of layers
+        // 1..nzl-1) -> finish -> unpack -> z faces of layers 0 and nzl
+        int rc = halo_pack(s, in);
+        if (rc) return rc;
+        const int which = in == s->qs ? 1 : 0;
+        if (s->nccl_on()) {
+            rc = nccl_exchange_start(s);
+            if (rc) return rc;
+        } else if (s->halo_start(s->halo_split_user, s, which) != 0) {
+            return fail(s, HGKS_ERR_CUDA, "halo exchange start callback failed");
+        }
+        ev_record(s, stage * 3 + 0);
+        s->ks.face_axis(kp, 0, in, s->face[0], s->stream, 0, s->nzl);
+        s->ks.face_axis(kp, 1, in, s->face[1], s->stream, 0, s->nzl);
+        s->ks.face_axis(kp, 2, in, s->face[2], s->stream, 1, s->nzl);
+        if (s->nccl_on()) {
+            rc = nccl_exchange_finish(s);
+            if (rc) return rc;
+        } else if (s->halo_finish(s->halo_split_user, s, which) != 0) {
+            return fail(s, HGKS_ERR_CUDA, "halo exchange finish callback failed");
+        }
+        rc = halo_unpack(s, in);
+        if (rc) return rc;
+        s->ks.face_axis(kp, 2, in, s->face[2], s->stream, 0, 1);
+        s->ks.face_axis(kp, 2, in, s->face[2], s->stream, s->nzl, kp.zface_layers);
+        s->launches += 5;
+    } else {
+        int rc = fill_ghosts(s, in);
+        if (rc) return rc;
+        ev_record(s, stage * 3 + 0);
+        s->ks.face(kp, in, s->face, s->stream, 0, nullptr);
+        s->launches += 3;
+    }
+    ev_record(s, stage * 3 + 1);
+    s->ks.cell(kp, mode, in, s->face, nullptr, s->A, nullptr, o0, o1, nullptr, s->stream, 0, nullptr);
+    s->launches += 1;
+    ev_record(s, stage * 3 + 2);
+    CK(cudaGetLastError());
+    return HGKS_OK;
+}
+
+// both stages of one S2O4 step from `in` into `out` with the scalars of `slot`
+int enqueue_stages(hgks_solver* s, double* in, double* out, int slot) {
+    // stage 1: q* = q + dt/2 L1 + dt^2/8 Lt1 and A = q + dt L1 + dt^2/6 Lt1
+    int rc = run_residual(s, in, 0, slot, MODE_STAGE1, s->qs, s->A);
+    if (rc) return rc;
+    // stage 2: q^{n+1} = A + dt^2/6 * 2 Lt2 (integrator.hpp:72-74)
+    return run_residual(s, s->qs, 1, slot, MODE_STAGE2, out, nullptr);
+}
+
+bool owns_item(hgks_solver* s, int phase, long item) {
+    const long nc = (long)s->nx * s->ny * s->nz;
+    const long cell = phase == 0 ? item % nc : item;
+    const long kg = cell / ((long)s->nx * s->ny);
+    return kg >= s->z0 && kg < s->z0 + s->nzl;
+}
+
+// The offending value of a (globally reduced) key: the slab that owns the item
+// re-runs the failing tile in report mode; the value is summed over slabs
+// (the others contribute 0), so every rank formats the same message.
+int report_value(hgks_solver* s, bool owner, const std::function<void()>& rerun, double* val) {
+    CK(cudaMemsetAsync(s->d_val, 0, sizeof(double), s->stream));
+    if (owner) rerun();
+    CK(cudaGetLastError());
+    if (s->nccl_on()) {
+        const int rc = nccl_reduce(s, s->d_val, 1, false);
+        if (rc) return rc;
+    }
+    CK(cudaMemcpyAsync(val, s->d_val, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    if (s->host_hooks() && s->hreduce && s->hreduce(s->hreduce_user, HGKS_REDUCE_SUM_F64, val, 1) != 0)
+        return fail(s, HGKS_ERR_CUDA, "host reduce callback failed");
+    return HGKS_OK;
+}
+
+// Decode the winning step key; shape the message as worker_error does
+// (runtime.hpp:37-41).
+int finish_error(hgks_solver* s, unsigned long long key, double* const stage_inputs[2], int slot) {
     const int stage = (int)(key >> 62) & 1;
     const int phase = (int)(key >> 61) & 1;
     const long item = (long)((key >> 22) & ((1ull << 39) - 1));
     const int code = (int)(key & 0xff);
-    KParams kp = make_params(s, dt, stage);
+    KParams kp = make_params(s, stage, slot);
     kp.report = 1;
     kp.count_fluxes = 0;
-    int tile[4];
     const long nc = (long)s->nx * s->ny * s->nz;
-    long cell = phase == 0 ? item % nc : item;
+    const long cell = phase == 0 ? item % nc : item;
     const int axis = phase == 0 ? (int)(item / nc) : 0;
     const int i = (int)(cell % s->nx), j = (int)((cell / s->nx) % s->ny);
     const int k = (int)(cell / ((long)s->nx * s->ny)) - s->z0;
-    double* nof[3] = {s->face[0], s->face[1], s->face[2]};
-    const double* in = stage_inputs[stage];
-    if (phase == 0) {
-        tile[0] = i / 32;
-        tile[1] = j;
-        tile[2] = k;
-        tile[3] = axis;
-        s->ks.face(kp, in, nof, s->stream, 1, tile);
-    } else {
-        tile[0] = i / s->ks.cell_tc;
-        tile[1] = j;
-        tile[2] = k;
-        tile[3] = 0;
-        s->ks.cell(kp, MODE_RESIDUAL, in, nof, nullptr, nullptr, nullptr, nullptr, nullptr,
-                   nullptr, s->stream, 1, tile);
-    }
-    CK(cudaGetLastError());
+    double* in = stage_inputs[stage];
     double val = 0.0;
-    CK(cudaMemcpyAsync(&val, s->d_val, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-    CK(cudaStreamSynchronize(s->stream));
+    const int rc = report_value(s, owns_item(s, phase, item), [&] {
+        int tile[4];
+        if (phase == 0) {
+            tile[0] = i / 32;
+            tile[1] = j;
+            tile[2] = k;
+            tile[3] = axis;
+            s->ks.face(kp, in, s->face, s->stream, 1, tile);
+        } else {
+            tile[0] = i / s->ks.cell_tc;
+            tile[1] = j;
+            tile[2] = k;
+            tile[3] = 0;
+            s->ks.cell(kp, MODE_RESIDUAL, in, s->face, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                       s->stream, 1, tile);
+        }
+    }, &val);
+    if (rc) return rc;
     s->e_code = HGKS_ERR_STATE;
     s->e_phase = phase;
     s->e_item = item;
@@ -254,61 +439,46 @@ int finish_error(hgks_solver* s, unsigned long long key, const double* stage_inp
     return HGKS_ERR_STATE;
 }
 
-void ev_record(hgks_solver* s, int i) {
-    if (s->timing) cudaEventRecord(s->ev[i], s->stream);
+// compute_dt's state failure: the bare state error (not wrapped in worker_error)
+int finish_dt_error(hgks_solver* s, unsigned long long key, const double* q, double cfl) {
+    const long item = (long)((key >> 22) & ((1ull << 39) - 1));
+    const int code = (int)(key & 0xff);
+    KParams kp = make_params(s, 0, 0);
+    kp.report = 1;
+    kp.err_key = s->d_key + K_DTERR;
+    double val = 0.0;
+    const int rc = report_value(s, owns_item(s, 1, item), [&] {
+        dt_kernel<<<148 * 4, 256, 0, s->stream>>>(kp, q, cfl, s->cfg.degree, s->d_key + K_SCRATCH);
+    }, &val);
+    if (rc) return rc;
+    s->e_code = HGKS_ERR_STATE;
+    s->e_phase = 2;
+    s->e_item = item;
+    s->e_value = val;
+    s->msg = code == ERR_DENSITY ? "non-positive density: rho=" + fmt_f(val) : "non-positive pressure: p=" + fmt_f(val);
+    return HGKS_ERR_STATE;
 }
 
-// One residual evaluation of `in` (ghosts filled here) in the given mode.
-int run_residual(hgks_solver* s, int which, double dt, int stage, int mode, const double* qn,
-                 double* o0, double* o1, double* o2) {
-    double* in = which_array(s, which);
-    KParams kp = make_params(s, dt, stage);
-    kp.ft_only = mode == MODE_STAGE2;
-    if (!s->single && !s->external_halo && s->halo_start) {
-        // overlapped halo: pack -> start the exchange -> faces that need no
-        // ghost (x, y faces of every owned layer, z faces of layers
-        // 1..nzl-1) -> finish -> unpack -> z faces of layers 0 and nzl
-        int rc = halo_pack(s, which);
+// After a host-dt step or residual: reduce the key over slabs, read it back,
+// report the globally first failure on every rank.
+int check_error(hgks_solver* s, double* const stage_inputs[2], int slot, bool* failed) {
+    *failed = false;
+    if (s->nccl_on()) {
+        const int rc = nccl_reduce(s, s->d_key + K_STEP, 1, true);
         if (rc) return rc;
-        if (s->halo_start(s->halo_split_user, s, which) != 0)
-            return fail(s, HGKS_ERR_CUDA, "halo exchange start callback failed");
-        ev_record(s, stage * 3 + 0);
-        s->ks.face_axis(kp, 0, in, s->face[0], s->stream, 0, s->nzl);
-        s->ks.face_axis(kp, 1, in, s->face[1], s->stream, 0, s->nzl);
-        s->ks.face_axis(kp, 2, in, s->face[2], s->stream, 1, s->nzl);
-        if (s->halo_finish(s->halo_split_user, s, which) != 0)
-            return fail(s, HGKS_ERR_CUDA, "halo exchange finish callback failed");
-        rc = halo_unpack(s, which);
-        if (rc) return rc;
-        s->ks.face_axis(kp, 2, in, s->face[2], s->stream, 0, 1);
-        s->ks.face_axis(kp, 2, in, s->face[2], s->stream, s->nzl, kp.zface_layers);
-        s->launches += 5;
-    } else {
-        int rc = fill_ghosts(s, which);
-        if (rc) return rc;
-        ev_record(s, stage * 3 + 0);
-        s->ks.face(kp, in, s->face, s->stream, 0, nullptr);
-        s->launches += 3;
     }
-    ev_record(s, stage * 3 + 1);
-    s->ks.cell(kp, mode, in, s->face, qn, s->A, nullptr, o0, o1, o2, s->stream, 0, nullptr);
-    s->launches += 1;
-    ev_record(s, stage * 3 + 2);
-    CK(cudaGetLastError());
-    return HGKS_OK;
-}
-
-int check_error(hgks_solver* s, const double* stage_inputs[2], double dt, bool* failed) {
-    unsigned long long h[3];
-    CK(cudaMemcpyAsync(h, s->d_key, sizeof h, cudaMemcpyDeviceToHost, s->stream));
+    unsigned long long h[2];  // K_STEP, K_FLUX
+    CK(cudaMemcpyAsync(h, s->d_key + K_STEP, sizeof h, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     if (s->count_fluxes) {
-        s->flux_evals += (long)h[2];
-        const unsigned long long z = 0;
-        CK(cudaMemcpyAsync(s->d_key + 2, &z, sizeof z, cudaMemcpyHostToDevice, s->stream));
+        s->flux_evals += (long)h[1];
+        CK(cudaMemsetAsync(s->d_key + K_FLUX, 0, sizeof(unsigned long long), s->stream));
     }
-    *failed = h[0] != ~0ull;
-    if (*failed) return finish_error(s, h[0], stage_inputs, dt);
+    if (s->host_hooks() && s->hreduce &&
+        s->hreduce(s->hreduce_user, HGKS_REDUCE_MIN_U64, &h[0], 1) != 0)
+        return fail(s, HGKS_ERR_CUDA, "host reduce callback failed");
+    *failed = h[0] != kNoKey;
+    if (*failed) return finish_error(s, h[0], stage_inputs, slot);
     return HGKS_OK;
 }
 
@@ -371,15 +541,18 @@ int hgks_create(const hgks_config* cfg, hgks_solver** out) {
     const long pad = 64;
     s->cs = ((s->S * (s->nzl + 2) + pad - 1) / pad) * pad;
     s->zface_layers = s->single ? s->nzl : s->nzl + 1;
-    s->fs = ((s->S * s->zface_layers + pad - 1) / pad) * pad;
+    // z-face buffers always hold nzl + 1 layers, so attaching a slab transport
+    // later (hgks_attach_nccl) needs no reallocation
+    s->fs = ((s->S * (s->nzl + 1) + pad - 1) / pad) * pad;
     cudaError_t ce;
     *out = s;
-    CK(cudaSetDevice(cfg->device));  // kernel attributes / occupancy below are per device
+    GUARD(s);  // kernel attributes / occupancy below are per device
     if (!pick_kernels(cfg->degree, cfg->dim, cfg->mu > 0.0, s->ks, ce)) return bad("no kernels for this degree/dim");
     if (ce != cudaSuccess) return cuda_fail(s, ce, "cudaFuncSetAttribute");
     CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     s->own_stream = true;
     for (auto& e : s->ev) CK(cudaEventCreate(&e));
+    for (auto& e : s->ev_stat) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     const size_t arr = (size_t)s->NC * s->cs * sizeof(double);
     CK(cudaMalloc(&s->d_tab, s->tabs.img.size() * sizeof(double)));
     CK(cudaMemcpy(s->d_tab, s->tabs.img.data(), s->tabs.img.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -401,7 +574,7 @@ int hgks_create(const hgks_config* cfg, hgks_solver** out) {
     CK(cudaMemcpy(s->d_dx, dx.data(), dx.size() * sizeof(double), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(s->d_dy, dy.data(), dy.size() * sizeof(double), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(s->d_dz, dz.data(), dz.size() * sizeof(double), cudaMemcpyHostToDevice));
-    for (double** p : {&s->qa, &s->qb, &s->qs, &s->A}) {
+    for (double** p : {&s->buf[0], &s->buf[1], &s->qs, &s->A}) {
         CK(cudaMalloc(p, arr));
         CK(cudaMemset(*p, 0, arr));
     }
@@ -410,10 +583,15 @@ int hgks_create(const hgks_config* cfg, hgks_solver** out) {
         CK(cudaMalloc(&s->face[a], fb));
         CK(cudaMemset(s->face[a], 0, fb));
     }
-    CK(cudaMalloc(&s->d_key, 4 * sizeof(unsigned long long)));
-    CK(cudaMemset(s->d_key, 0, 4 * sizeof(unsigned long long)));
+    CK(cudaMalloc(&s->d_key, K_WORDS * sizeof(unsigned long long)));
+    CK(cudaMemset(s->d_key, 0, K_WORDS * sizeof(unsigned long long)));
     CK(cudaMalloc(&s->d_val, 4 * sizeof(double)));
     CK(cudaMalloc(&s->d_red, 4096 * sizeof(double)));
+    CK(cudaMalloc(&s->d_scal, 2 * SC_SLOT * sizeof(double)));
+    CK(cudaMemset(s->d_scal, 0, 2 * SC_SLOT * sizeof(double)));
+    CK(cudaMalloc(&s->d_ctl, sizeof(StepCtl)));
+    CK(cudaMalloc(&s->d_stat, sizeof(StepStatus)));
+    CK(cudaMallocHost(&s->h_stat, 2 * sizeof(StepStatus)));
     CK(cudaMalloc(&s->d_halo, 4 * (size_t)s->S * s->NC * sizeof(double)));
     CK(cudaMemset(s->d_halo, 0, 4 * (size_t)s->S * s->NC * sizeof(double)));
     return HGKS_OK;
@@ -421,17 +599,29 @@ int hgks_create(const hgks_config* cfg, hgks_solver** out) {
 
 void hgks_destroy(hgks_solver* s) {
     if (!s) return;
-    for (double* p : {s->d_tab, s->d_dx, s->d_dy, s->d_dz, s->qa, s->qb, s->qs, s->A,
-                      s->R, s->Rt, s->tmp, s->tmp2, s->face[0], s->face[1], s->face[2], s->d_val, s->d_red,
-                      s->d_halo})
+    GUARD(s);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    drop_graphs(s);
+    if (s->comm && s->own_comm) nccl().CommDestroy(s->comm);
+    for (double* p : {s->d_tab, s->d_dx, s->d_dy, s->d_dz, s->buf[0], s->buf[1], s->qs, s->A, s->R, s->Rt,
+                      s->tmp, s->tmp2, s->face[0], s->face[1], s->face[2], s->d_val, s->d_red, s->d_halo,
+                      s->d_scal})
         if (p) cudaFree(p);
     if (s->d_key) cudaFree(s->d_key);
+    if (s->d_ctl) cudaFree(s->d_ctl);
+    if (s->d_stat) cudaFree(s->d_stat);
+    if (s->h_stat) cudaFreeHost(s->h_stat);
     for (auto& e : s->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : s->ev_stat)
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {s->ev_pack, s->ev_xfer})
         if (e) cudaEventDestroy(e);
     for (auto* v : {&s->ev_up, &s->ev_c2, &s->ev_dn})
         for (auto e : *v) cudaEventDestroy(e);
     if (s->st_up) cudaStreamDestroy(s->st_up);
     if (s->st_dn) cudaStreamDestroy(s->st_dn);
+    if (s->st_comm) cudaStreamDestroy(s->st_comm);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
 }
@@ -464,7 +654,7 @@ int upload_aos(hgks_solver* s, const double* host, double* dst) {
     if (rc) return rc;
     const size_t n = (size_t)hgks_num_coeffs(s);
     CK(cudaMemcpyAsync(s->tmp, host, n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
-    KParams kp = make_params(s, 0.0, 0);
+    KParams kp = make_params(s, 0, 0);
     aos_to_soa_kernel<<<(int)std::min<long>(((long)n + 255) / 256, 148L * 32), 256, 0, s->stream>>>(
         kp, s->tmp, dst, s->NC);
     ++s->launches;
@@ -476,7 +666,7 @@ int download_aos(hgks_solver* s, const double* src, double* host) {
     int rc = ensure_tmp(s);
     if (rc) return rc;
     const size_t n = (size_t)hgks_num_coeffs(s);
-    KParams kp = make_params(s, 0.0, 0);
+    KParams kp = make_params(s, 0, 0);
     soa_to_aos_kernel<<<(int)std::min<long>(((long)n + 255) / 256, 148L * 32), 256, 0, s->stream>>>(
         kp, src, s->tmp, s->NC);
     ++s->launches;
@@ -498,22 +688,24 @@ int download_faces(hgks_solver* s, int axis, double* host) {
     return HGKS_OK;
 }
 
+// host-dt step in three phases (hgks_step, hgks_step_phase): 0 = stage 1,
+// 1 = stage 2 (into buf[cur^1]), 2 = error check + commit (flip cur)
 int step_phase(hgks_solver* s, double dt, int phase) {
     int rc;
     if (phase == 0) {
-        // stage 1: q* and A from q^n (qa)
-        rc = reset_error(s);
+        rc = reset_keys(s);
         if (rc) return rc;
-        return run_residual(s, 0, dt, 0, MODE_STAGE1, nullptr, s->qs, s->A, nullptr);
+        rc = set_scalars(s, 0, dt);
+        if (rc) return rc;
+        return run_residual(s, s->qa(), 0, 0, MODE_STAGE1, s->qs, s->A);
     }
-    if (phase == 1)  // stage 2: q^{n+1} into qb from q* and A
-        return run_residual(s, 1, dt, 1, MODE_STAGE2, s->qa, s->qb, nullptr, nullptr);
-    const double* inputs[2] = {s->qa, s->qs};
+    if (phase == 1) return run_residual(s, s->qs, 1, 0, MODE_STAGE2, s->qb(), nullptr);
+    double* const inputs[2] = {s->qa(), s->qs};
     bool failed = false;
-    rc = check_error(s, inputs, dt, &failed);
+    rc = check_error(s, inputs, 0, &failed);
     if (rc) return rc;
     collect_times(s, 2);
-    std::swap(s->qa, s->qb);
+    s->cur ^= 1;
     s->time += dt;
     return HGKS_OK;
 }
@@ -526,12 +718,234 @@ int do_step(hgks_solver* s, double dt) {
     return HGKS_OK;
 }
 
+int compute_dt_host(hgks_solver* s, double cfl, double* dt) {
+    int rc = reset_keys(s);
+    if (rc) return rc;
+    KParams kp = make_params(s, 0, 0);
+    kp.err_key = s->d_key + K_DTERR;
+    dt_kernel<<<148 * 4, 256, 0, s->stream>>>(kp, s->qa(), cfl, s->cfg.degree, s->d_key + K_DT);
+    ++s->launches;
+    CK(cudaGetLastError());
+    if (s->nccl_on()) {  // (dt error key, dt bits) min over slabs in one call
+        rc = nccl_reduce(s, s->d_key + K_DTERR, 2, true);
+        if (rc) return rc;
+    }
+    unsigned long long h[2];  // K_DTERR, K_DT
+    CK(cudaMemcpyAsync(h, s->d_key + K_DTERR, sizeof h, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    // every rank joins the reduction, also one whose own cells failed (no rank
+    // is left waiting in the next collective)
+    if (s->host_hooks() && s->hreduce && s->hreduce(s->hreduce_user, HGKS_REDUCE_MIN_U64, h, 2) != 0)
+        return fail(s, HGKS_ERR_CUDA, "host reduce callback failed");
+    if (h[0] != kNoKey) return finish_dt_error(s, h[0], s->qa(), cfl);
+    double v;
+    std::memcpy(&v, &h[1], sizeof v);
+    if (!(v > 0.0) || !std::isfinite(v)) return fail(s, HGKS_ERR_DT, "compute_dt: nonpositive dt");
+    *dt = v;
+    return HGKS_OK;
+}
+
+// ---- device-resident advance loop
+// One step with dt from the device: [dt kernel + slab min] -> dt_finalize
+// (clip, halt) -> both stages -> [slab min of the step key] -> commit ->
+// status to pinned memory. Reads buf[p], writes buf[p^1], scalars slot p.
+int enqueue_device_step(hgks_solver* s, int p, double cfl, bool fixed) {
+    if (!fixed) {
+        KParams kp = make_params(s, 0, p);
+        kp.err_key = s->d_key + K_DTERR;
+        dt_kernel<<<148 * 4, 256, 0, s->stream>>>(kp, s->buf[p], cfl, s->cfg.degree, s->d_key + K_DT);
+        ++s->launches;
+        if (s->nccl_on()) {
+            const int rc = nccl_reduce(s, s->d_key + K_DTERR, 2, true);
+            if (rc) return rc;
+        }
+    }
+    dt_finalize_kernel<<<1, 1, 0, s->stream>>>(s->d_ctl, s->d_key, scal_slot(s, p));
+    ++s->launches;
+    int rc = enqueue_stages(s, s->buf[p], s->buf[p ^ 1], p);
+    if (rc) return rc;
+    if (s->nccl_on()) {
+        rc = nccl_reduce(s, s->d_key + K_STEP, 1, true);
+        if (rc) return rc;
+    }
+    commit_kernel<<<1, 1, 0, s->stream>>>(s->d_ctl, s->d_key, scal_slot(s, p), s->d_stat);
+    ++s->launches;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s->h_stat + p, s->d_stat, sizeof(StepStatus), cudaMemcpyDeviceToHost, s->stream));
+    return HGKS_OK;
+}
+
+int ensure_graphs(hgks_solver* s, double cfl, bool fixed) {
+    if (s->gexec[0] && s->g_cfl == cfl && s->g_fixed == (int)fixed) return HGKS_OK;
+    drop_graphs(s);
+    for (int p = 0; p < 2; ++p) {
+        cudaGraph_t g = nullptr;
+        const long l0 = s->launches;
+        CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+        const int rc = enqueue_device_step(s, p, cfl, fixed);
+        const cudaError_t ce = cudaStreamEndCapture(s->stream, &g);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        CK(ce);
+        CK(cudaGraphInstantiate(&s->gexec[p], g, 0));
+        cudaGraphDestroy(g);
+        s->glaunches[p] = s->launches - l0;
+        s->launches = l0;
+    }
+    s->g_cfl = cfl;
+    s->g_fixed = fixed;
+    return HGKS_OK;
+}
+
+// advance (solver.hpp:62-108) with the whole step on the device. The host
+// runs one step ahead: it launches step n+1 before it reads step n's status,
+// so the GPU never waits for the host. A step after the loop halted (t_end
+// reached, state error, bad dt) is a no-op on the device; q^n of the failing
+// step is intact in buf[n parity].
+int advance_device(hgks_solver* s, double t_end, double cfl, double dt_fixed, double record_interval,
+                   double first_record, int max_steps, hgks_record_fn on_record, void* user, int* steps) {
+    const bool fixed = dt_fixed > 0.0;
+    StepCtl c{};
+    c.t = s->time;
+    c.t_end = t_end;
+    c.record_interval = record_interval;
+    c.next_record = first_record;
+    c.record = record_interval > 0.0 ? 1 : 0;
+    c.dt_fixed = fixed ? dt_fixed : 0.0;
+    c.mu = s->cfg.mu;
+    c.fail_key = kNoKey;
+    CK(cudaMemcpyAsync(s->d_ctl, &c, sizeof c, cudaMemcpyHostToDevice, s->stream));
+    int rc = reset_keys(s);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(s->stream));  // c and the key init are on the stack / static
+    const bool graphs = s->use_graphs && !s->timing;
+    if (graphs && (rc = ensure_graphs(s, cfl, fixed))) return rc;
+    const int p0 = s->cur;
+    long sub = 0, done = 0;
+    auto launch = [&](long n) -> int {
+        const int p = (int)((p0 + n) & 1);
+        if (graphs) {
+            CK(cudaGraphLaunch(s->gexec[p], s->stream));
+            s->launches += s->glaunches[p];
+        } else {
+            const int r = enqueue_device_step(s, p, cfl, fixed);
+            if (r) return r;
+        }
+        CK(cudaEventRecord(s->ev_stat[p], s->stream));
+        return HGKS_OK;
+    };
+    StepStatus last{};
+    last.t = s->time;
+    int halted = HALT_NONE;
+    long halt_step = -1;
+    bool stop_launch = false;
+    while (true) {
+        if (!stop_launch && (max_steps <= 0 || sub < max_steps)) {
+            rc = launch(sub++);
+            if (rc) return rc;
+        } else {
+            stop_launch = true;
+        }
+        if (done == sub) break;
+        if (sub - done < 2 && !stop_launch) continue;
+        // status of step `done` (one step behind the launches)
+        const int p = (int)((p0 + done) & 1);
+        CK(cudaEventSynchronize(s->ev_stat[p]));
+        const StepStatus st = s->h_stat[p];
+        if (st.halted != HALT_NONE) {
+            halted = st.halted;
+            halt_step = done;
+            last = st;
+            break;
+        }
+        last = st;
+        ++done;
+        if (st.rec_hit && on_record) {
+            // the record state is this step's output, buf[(p0 + done) & 1];
+            // the step in flight only reads it
+            s->cur = (int)((p0 + done) & 1);
+            s->time = st.t;
+            if (on_record(user, s, st.t) != 0) {
+                CK(cudaStreamSynchronize(s->stream));
+                return fail(s, HGKS_ERR_CONFIG, "on_record callback failed");
+            }
+        }
+    }
+    CK(cudaStreamSynchronize(s->stream));
+    if (s->count_fluxes) {
+        unsigned long long fc = 0;
+        CK(cudaMemcpy(&fc, s->d_key + K_FLUX, sizeof fc, cudaMemcpyDeviceToHost));
+        s->flux_evals += (long)fc;
+        CK(cudaMemset(s->d_key + K_FLUX, 0, sizeof fc));
+    }
+    if (halted == HALT_NONE) {
+        s->cur = (int)((p0 + done) & 1);
+        s->time = last.t;
+        if (steps) *steps = last.steps;
+        return HGKS_OK;
+    }
+    // the halting step's input is q^n (also for HALT_DONE: that step was a no-op)
+    const int ph = (int)((p0 + halt_step) & 1);
+    s->cur = ph;
+    s->time = last.t;
+    if (steps) *steps = last.steps;
+    if (halted == HALT_DONE) return HGKS_OK;
+    if (halted == HALT_DT) return fail(s, HGKS_ERR_DT, "compute_dt: nonpositive dt");
+    if (halted == HALT_DT_STATE) return finish_dt_error(s, last.fail_key, s->buf[ph], cfl);
+    double* const inputs[2] = {s->buf[ph], s->qs};
+    rc = finish_error(s, last.fail_key, inputs, ph);
+    if (rc == HGKS_ERR_STATE) s->msg += " at t=" + std::to_string(last.t);
+    return rc;
+}
+
+// the same loop with host-side dt (host transports: the dt / key reductions
+// and halo exchanges are callbacks)
+int advance_host(hgks_solver* s, double t_end, double cfl, double dt_fixed, double record_interval,
+                 double first_record, int max_steps, hgks_record_fn on_record, void* user, int* steps) {
+    double t = s->time;
+    double next_record = first_record;
+    int n = 0;
+    while (t < t_end - 1e-14 * t_end && (max_steps <= 0 || n < max_steps)) {
+        double dt = dt_fixed;
+        if (!(dt_fixed > 0.0)) {
+            const int rc = compute_dt_host(s, cfl, &dt);
+            if (rc) {
+                if (steps) *steps = n;
+                return rc;
+            }
+        }
+        dt = std::min(dt, t_end - t);
+        if (record_interval > 0) dt = std::min(dt, next_record - t);
+        const int rc = do_step(s, dt);
+        if (rc) {
+            if (rc == HGKS_ERR_STATE) s->msg += " at t=" + std::to_string(t);
+            if (steps) *steps = n;
+            return rc;
+        }
+        t += dt;
+        s->time = t;
+        ++n;
+        if (record_interval > 0 && t >= next_record - 1e-12) {
+            next_record += record_interval;
+            if (on_record && on_record(user, s, t) != 0) {
+                if (steps) *steps = n;
+                return fail(s, HGKS_ERR_CONFIG, "on_record callback failed");
+            }
+        }
+    }
+    if (steps) *steps = n;
+    return HGKS_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
 int hgks_set_state(hgks_solver* s, const double* coeffs, double time) {
-    const int rc = upload_aos(s, coeffs, s->qa);
+    GUARD(s);
+    const int rc = upload_aos(s, coeffs, s->qa());
     if (rc) return rc;
     s->time = time;
     CK(cudaStreamSynchronize(s->stream));
@@ -539,30 +953,33 @@ int hgks_set_state(hgks_solver* s, const double* coeffs, double time) {
 }
 
 int hgks_get_state(hgks_solver* s, double* coeffs, double* time) {
+    GUARD(s);
     if (time) *time = s->time;
-    return coeffs ? download_aos(s, s->qa, coeffs) : HGKS_OK;
+    return coeffs ? download_aos(s, s->qa(), coeffs) : HGKS_OK;
 }
 
 int hgks_residual(hgks_solver* s, const double* coeffs, double dt, double* R, double* Rt,
                   double* face0, double* face1, double* face2) {
+    GUARD(s);
     const size_t arr = (size_t)s->NC * s->cs * sizeof(double);
     if (!s->R) CK(cudaMalloc(&s->R, arr));
     if (!s->Rt) CK(cudaMalloc(&s->Rt, arr));
-    int which = 0;
     int rc;
+    double* in = s->qa();
     if (coeffs) {
         rc = upload_aos(s, coeffs, s->qs);
         if (rc) return rc;
-        which = 1;
+        in = s->qs;
     }
-    const double* in = which_array(s, which);
-    rc = reset_error(s);
+    rc = reset_keys(s);
     if (rc) return rc;
-    rc = run_residual(s, which, dt, 0, MODE_RESIDUAL, nullptr, s->R, s->Rt, nullptr);
+    rc = set_scalars(s, 0, dt);
     if (rc) return rc;
-    const double* inputs[2] = {in, in};
+    rc = run_residual(s, in, 0, 0, MODE_RESIDUAL, s->R, s->Rt);
+    if (rc) return rc;
+    double* const inputs[2] = {in, in};
     bool failed = false;
-    rc = check_error(s, inputs, dt, &failed);
+    rc = check_error(s, inputs, 0, &failed);
     if (rc) return rc;
     collect_times(s, 1);
     if (R && (rc = download_aos(s, s->R, R))) return rc;
@@ -574,9 +991,10 @@ int hgks_residual(hgks_solver* s, const double* coeffs, double dt, double* R, do
 }
 
 int hgks_apply_inverse_mass(hgks_solver* s, const double* R, double* L) {
+    GUARD(s);
     int rc = upload_aos(s, R, s->qs);
     if (rc) return rc;
-    KParams kp = make_params(s, 0.0, 0);
+    KParams kp = make_params(s, 0, 0);
     const long n = hgks_num_coeffs(s);
     inverse_mass_kernel<<<(int)std::min<long>((n + 255) / 256, 148L * 32), 256, 0, s->stream>>>(
         kp, s->qs, s->NC);
@@ -586,50 +1004,22 @@ int hgks_apply_inverse_mass(hgks_solver* s, const double* R, double* L) {
 }
 
 int hgks_compute_dt(hgks_solver* s, double cfl, double* dt) {
-    int rc = reset_error(s);
-    if (rc) return rc;
-    KParams kp = make_params(s, 0.0, 0);
-    dt_kernel<<<148 * 4, 256, 0, s->stream>>>(kp, s->qa, cfl, s->cfg.degree, s->d_key + 1);
-    ++s->launches;
-    CK(cudaGetLastError());
-    unsigned long long h[2];
-    CK(cudaMemcpyAsync(h, s->d_key, sizeof h, cudaMemcpyDeviceToHost, s->stream));
-    CK(cudaStreamSynchronize(s->stream));
-    if (h[0] != ~0ull) {
-        // compute_dt throws the bare state error, not wrapped in worker_error
-        const long item = (long)((h[0] >> 22) & ((1ull << 39) - 1));
-        const int code = (int)(h[0] & 0xff);
-        kp.report = 1;
-        dt_kernel<<<148 * 4, 256, 0, s->stream>>>(kp, s->qa, cfl, s->cfg.degree, s->d_key + 3);
-        double val = 0;
-        CK(cudaMemcpyAsync(&val, s->d_val, sizeof val, cudaMemcpyDeviceToHost, s->stream));
-        CK(cudaStreamSynchronize(s->stream));
-        s->e_code = HGKS_ERR_STATE;
-        s->e_phase = 2;
-        s->e_item = item;
-        s->e_value = val;
-        s->msg = code == ERR_DENSITY ? "non-positive density: rho=" + fmt_f(val)
-                                     : "non-positive pressure: p=" + fmt_f(val);
-        return HGKS_ERR_STATE;
-    }
-    double v;
-    std::memcpy(&v, &h[1], sizeof v);
-    if (s->dtmin) {
-        if (s->dtmin(s->dtmin_user, &v) != 0) return fail(s, HGKS_ERR_CUDA, "dt reduction callback failed");
-    }
-    if (!(v > 0.0) || !std::isfinite(v)) return fail(s, HGKS_ERR_DT, "compute_dt: nonpositive dt");
-    *dt = v;
-    return HGKS_OK;
+    GUARD(s);
+    return compute_dt_host(s, cfl, dt);
 }
 
-int hgks_step(hgks_solver* s, double dt) { return do_step(s, dt); }
+int hgks_step(hgks_solver* s, double dt) {
+    GUARD(s);
+    return do_step(s, dt);
+}
 
 int hgks_two_stage_step_host(hgks_solver* s, double* q, double dt) {
-    int rc = upload_aos(s, q, s->qa);
+    GUARD(s);
+    int rc = upload_aos(s, q, s->qa());
     if (rc) return rc;
     rc = do_step(s, dt);
     if (rc) return rc;
-    return download_aos(s, s->qa, q);
+    return download_aos(s, s->qa(), q);
 }
 
 int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int nchunks) {
@@ -643,6 +1033,7 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
     //            last chunk's q*, so it closes the wavefront)
     //   downloads (copy stream): D(1), ..., D(N-1), D(0) after their C2.
     // Stage 1 of chunk c needs U(c-1..c+1); its stage 2 needs C1(c-1..c+1).
+    GUARD(s);
     if (!s->single || nchunks <= 1 || s->nzl < 4) return hgks_two_stage_step_host(s, q, dt);
     const int N = std::min(nchunks, s->nzl / 2);
     int rc = ensure_tmp(s);
@@ -663,16 +1054,18 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
     auto kb = [&](int c) { return (int)((long)c * s->nzl / N); };
     const long S = s->S;
     const int NC = s->NC;
-    KParams kp0 = make_params(s, 0.0, 0);
+    KParams kp0 = make_params(s, 0, 0);
     const int tblocks = 148 * 8;
     // the previous call's downloads must be done before tmp2 / q are reused
     CK(cudaStreamSynchronize(s->st_dn));
-    rc = reset_error(s);
+    rc = reset_keys(s);
+    if (rc) return rc;
+    rc = set_scalars(s, 0, dt);
     if (rc) return rc;
     // ---- uploads
     cudaEvent_t start;
     CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-    CK(cudaEventRecord(start, s->stream));  // after reset_error on the compute stream
+    CK(cudaEventRecord(start, s->stream));  // after reset_keys on the compute stream
     CK(cudaStreamWaitEvent(s->st_up, start, 0));
     // the copy streams carry only copies (the AoS <-> SoA transposes run on
     // the compute stream), so the copy engines never wait for an SM slot
@@ -686,11 +1079,13 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
     }
     cudaEventDestroy(start);
     // ---- compute wavefront
-    const KParams kp1 = make_params(s, dt, 0);
-    KParams kp2 = make_params(s, dt, 1);
+    const KParams kp1 = make_params(s, 0, 0);
+    KParams kp2 = make_params(s, 1, 0);
     kp2.ft_only = 1;
     const KernelSet& K = s->ks;
     cudaStream_t cs = s->stream;
+    double* qn = s->qa();
+    double* qnew = s->qb();
     // chunk c's upload landed -> transpose it into the SoA state (compute stream)
     std::vector<char> landed(N, 0);
     auto wait_up = [&](int c) {
@@ -699,22 +1094,22 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
         landed[c] = 1;
         const cudaError_t e = cudaStreamWaitEvent(cs, s->ev_up[c], 0);
         if (e != cudaSuccess) return e;
-        aos_to_soa_kernel<<<tblocks, 256, 0, cs>>>(kp0, s->tmp, s->qa, NC, kb(c) * S, kb(c + 1) * S);
+        aos_to_soa_kernel<<<tblocks, 256, 0, cs>>>(kp0, s->tmp, qn, NC, kb(c) * S, kb(c + 1) * S);
         ++s->launches;
         return cudaGetLastError();
     };
-    auto F1 = [&](int c) { K.face_layers(kp1, s->qa, s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
+    auto F1 = [&](int c) { K.face_layers(kp1, qn, s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
     auto C1 = [&](int c) {
-        K.cell_layers(kp1, MODE_STAGE1, s->qa, s->face, nullptr, nullptr, nullptr, s->qs, s->A, nullptr, cs,
+        K.cell_layers(kp1, MODE_STAGE1, qn, s->face, nullptr, nullptr, nullptr, s->qs, s->A, nullptr, cs,
                       kb(c), kb(c + 1));
         ++s->launches;
     };
     auto F2 = [&](int c) { K.face_layers(kp2, s->qs, s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
     auto C2 = [&](int c) {
-        K.cell_layers(kp2, MODE_STAGE2, s->qs, s->face, nullptr, s->A, nullptr, s->qb, nullptr, nullptr, cs,
+        K.cell_layers(kp2, MODE_STAGE2, s->qs, s->face, nullptr, s->A, nullptr, qnew, nullptr, nullptr, cs,
                       kb(c), kb(c + 1));
         // q^{n+1} of chunk c -> AoS staging for its download
-        soa_to_aos_kernel<<<tblocks, 256, 0, cs>>>(kp0, s->qb, s->tmp2, NC, kb(c) * S, kb(c + 1) * S);
+        soa_to_aos_kernel<<<tblocks, 256, 0, cs>>>(kp0, qnew, s->tmp2, NC, kb(c) * S, kb(c + 1) * S);
         s->launches += 2;
         return cudaEventRecord(s->ev_c2[c], cs);
     };
@@ -724,7 +1119,7 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
     };
     CK(wait_up(N - 1));
     CK(wait_up(0));
-    ghost(s->qa);
+    ghost(qn);
     F1(0);
     for (int i = 0; i < N; ++i) {
         if (i + 1 <= N - 1) {
@@ -749,47 +1144,45 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
                            cudaMemcpyDeviceToHost, s->st_dn));
     }
     CK(cudaStreamSynchronize(s->st_dn));
-    const double* inputs[2] = {s->qa, s->qs};
+    double* const inputs[2] = {qn, s->qs};
     bool failed = false;
-    rc = check_error(s, inputs, dt, &failed);
-    if (rc) return rc;  // q holds a partially advanced state (documented in the header)
-    std::swap(s->qa, s->qb);
+    rc = check_error(s, inputs, 0, &failed);
+    if (failed) {
+        // the reference's two_stage_step leaves q untouched on failure
+        // (integrator.hpp:72-74 run only after both evals): restore q^n from
+        // the upload staging buffer, which still holds it in full
+        CK(cudaMemcpyAsync(q, s->tmp, (size_t)hgks_num_coeffs(s) * sizeof(double), cudaMemcpyDeviceToHost,
+                           s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+    }
+    if (rc) return rc;
+    s->cur ^= 1;
     s->time += dt;
     return HGKS_OK;
 }
 
+int hgks_advance_records(hgks_solver* s, double t_end, double cfl, double dt_fixed, double record_interval,
+                         double first_record, int max_steps, hgks_record_fn on_record, void* user,
+                         int* steps) {
+    GUARD(s);
+    if (steps) *steps = 0;
+    if (s->host_hooks())
+        return advance_host(s, t_end, cfl, dt_fixed, record_interval, first_record, max_steps, on_record, user,
+                            steps);
+    return advance_device(s, t_end, cfl, dt_fixed, record_interval, first_record, max_steps, on_record, user,
+                          steps);
+}
+
 int hgks_advance(hgks_solver* s, double t_end, double cfl, double dt_fixed, double record_interval,
                  int* steps) {
-    double t = s->time;
-    double next_record = record_interval > 0 ? (std::floor(t / record_interval + 1e-9) + 1) * record_interval : 0;
-    int n = 0;
-    while (t < t_end - 1e-14 * t_end) {
-        double dt = dt_fixed;
-        if (!(dt_fixed > 0.0)) {
-            const int rc = hgks_compute_dt(s, cfl, &dt);
-            if (rc) {
-                if (steps) *steps = n;
-                return rc;
-            }
-        }
-        dt = std::min(dt, t_end - t);
-        if (record_interval > 0) dt = std::min(dt, next_record - t);
-        const int rc = do_step(s, dt);
-        if (rc) {
-            if (rc == HGKS_ERR_STATE) s->msg += " at t=" + std::to_string(t);
-            if (steps) *steps = n;
-            return rc;
-        }
-        t += dt;
-        s->time = t;
-        ++n;
-        if (record_interval > 0 && t >= next_record - 1e-12) next_record += record_interval;
-    }
-    if (steps) *steps = n;
-    return HGKS_OK;
+    const double t = s->time;
+    const double first =
+        record_interval > 0 ? (std::floor(t / record_interval + 1e-9) + 1) * record_interval : 0.0;
+    return hgks_advance_records(s, t_end, cfl, dt_fixed, record_interval, first, 0, nullptr, nullptr, steps);
 }
 
 void hgks_set_count_fluxes(hgks_solver* s, int on) {
+    if (s->count_fluxes != (on != 0)) drop_graphs(s);
     s->count_fluxes = on != 0;
     s->flux_evals = 0;
 }
@@ -813,6 +1206,7 @@ int case_setup(hgks_solver* s, const char* case_name, double t, CaseParams& cp, 
     for (int k = 0; k < s->nzl; ++k) ctr.push_back(0.5 * (s->zs[s->z0 + k] + s->zs[s->z0 + k + 1]));
     CK(cudaMalloc(d_ctr, ctr.size() * sizeof(double)));
     CK(cudaMemcpyAsync(*d_ctr, ctr.data(), ctr.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    CK(cudaStreamSynchronize(s->stream));  // ctr is a host temporary
     cp.cid = cid;
     cp.dim = s->cfg.dim;
     cp.gamma = s->cfg.gamma;
@@ -827,12 +1221,13 @@ int case_setup(hgks_solver* s, const char* case_name, double t, CaseParams& cp, 
 extern "C" {
 
 int hgks_project_case(hgks_solver* s, const char* case_name, double t) {
+    GUARD(s);
     CaseParams cp;
     double* d_ctr = nullptr;
     int rc = case_setup(s, case_name, t, cp, &d_ctr);
     if (rc) return rc;
-    KParams kp = make_params(s, 0.0, 0);
-    launch_project(s->cfg.degree, s->cfg.dim, kp, cp, d_ctr, s->qa, s->S * s->nzl, s->stream);
+    KParams kp = make_params(s, 0, 0);
+    launch_project(s->cfg.degree, s->cfg.dim, kp, cp, d_ctr, s->qa(), s->S * s->nzl, s->stream);
     ++s->launches;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s->stream));
@@ -842,14 +1237,15 @@ int hgks_project_case(hgks_solver* s, const char* case_name, double t) {
 }
 
 int hgks_error_norms(hgks_solver* s, const char* case_name, double t, double* out) {
+    GUARD(s);
     if (!std::strcmp(case_name, "tgv")) return fail(s, HGKS_ERR_CONFIG, "case has no exact solution: tgv");
     CaseParams cp;
     double* d_ctr = nullptr;
     int rc = case_setup(s, case_name, t, cp, &d_ctr);
     if (rc) return rc;
-    KParams kp = make_params(s, 0.0, 0);
+    KParams kp = make_params(s, 0, 0);
     const int blocks = 148 * 2;
-    launch_error(s->cfg.degree, s->cfg.dim, kp, cp, d_ctr, s->qa, s->S * s->nzl, s->d_red, blocks, s->stream);
+    launch_error(s->cfg.degree, s->cfg.dim, kp, cp, d_ctr, s->qa(), s->S * s->nzl, s->d_red, blocks, s->stream);
     ++s->launches;
     CK(cudaGetLastError());
     std::vector<double> part(3 * blocks);
@@ -869,10 +1265,11 @@ int hgks_error_norms(hgks_solver* s, const char* case_name, double t, double* ou
 }
 
 int hgks_tgv_diagnostics(hgks_solver* s, double* ek_vol, double* ens_vol, double* volume) {
-    KParams kp = make_params(s, 0.0, 0);
+    GUARD(s);
+    KParams kp = make_params(s, 0, 0);
     const long ncell = s->S * s->nzl;
     const int blocks = 148 * 2;
-    launch_tgv(s->cfg.degree, s->cfg.dim, kp, s->tabs.proj.npts, s->qa, ncell, s->d_red, blocks, s->stream);
+    launch_tgv(s->cfg.degree, s->cfg.dim, kp, s->tabs.proj.npts, s->qa(), ncell, s->d_red, blocks, s->stream);
     ++s->launches;
     CK(cudaGetLastError());
     std::vector<double> part(3 * blocks);
@@ -902,11 +1299,18 @@ int hgks_halo_buffers(hgks_solver* s, unsigned long long* send_lo, unsigned long
     return HGKS_OK;
 }
 
-int hgks_halo_pack(hgks_solver* s, int which) { return halo_pack(s, which); }
-int hgks_halo_unpack(hgks_solver* s, int which) { return halo_unpack(s, which); }
+int hgks_halo_pack(hgks_solver* s, int which) {
+    GUARD(s);
+    return halo_pack(s, which == 0 ? s->qa() : s->qs);
+}
+int hgks_halo_unpack(hgks_solver* s, int which) {
+    GUARD(s);
+    return halo_unpack(s, which == 0 ? s->qa() : s->qs);
+}
 
 int hgks_step_phase(hgks_solver* s, double dt, int phase) {
     if (phase < 0 || phase > 2) return fail(s, HGKS_ERR_CONFIG, "hgks_step_phase: phase must be 0, 1 or 2");
+    GUARD(s);
     s->external_halo = true;
     const int rc = step_phase(s, dt, phase);
     s->external_halo = false;
@@ -924,12 +1328,81 @@ void hgks_set_halo_exchange_split(hgks_solver* s, hgks_halo_fn start, hgks_halo_
     s->halo_split_user = user;
 }
 
-void hgks_set_dt_reduce(hgks_solver* s, hgks_min_fn fn, void* user) {
-    s->dtmin = fn;
-    s->dtmin_user = user;
+void hgks_set_host_reduce(hgks_solver* s, hgks_reduce_fn fn, void* user) {
+    s->hreduce = fn;
+    s->hreduce_user = user;
+}
+
+int hgks_nccl_unique_id(char* id_out, int nbytes) {
+    const NcclApi& N = nccl();
+    if (!N.ok) return HGKS_ERR_CUDA;
+    if (nbytes < (int)sizeof(ncclUniqueId)) return HGKS_ERR_CONFIG;
+    ncclUniqueId id;
+    if (N.GetUniqueId(&id) != ncclSuccess) return HGKS_ERR_CUDA;
+    std::memcpy(id_out, &id, sizeof id);
+    return HGKS_OK;
+}
+
+static int attach_common(hgks_solver* s, int rank, int world) {
+    // the slab ring always exchanges (world 1: the slab sends to itself),
+    // including z faces of both slab boundaries
+    s->rank = rank;
+    s->world = world;
+    s->single = false;
+    s->zface_layers = s->nzl + 1;
+    if (!s->st_comm) CK(cudaStreamCreateWithFlags(&s->st_comm, cudaStreamNonBlocking));
+    if (!s->ev_pack) CK(cudaEventCreateWithFlags(&s->ev_pack, cudaEventDisableTiming));
+    if (!s->ev_xfer) CK(cudaEventCreateWithFlags(&s->ev_xfer, cudaEventDisableTiming));
+    drop_graphs(s);
+    return HGKS_OK;
+}
+
+int hgks_attach_nccl(hgks_solver* s, const char* unique_id, int rank, int world) {
+    GUARD(s);
+    const NcclApi& N = nccl();
+    if (!N.ok) return fail(s, HGKS_ERR_CUDA, "NCCL unavailable: " + N.why);
+    if (world < 1 || rank < 0 || rank >= world)
+        return fail(s, HGKS_ERR_CONFIG, "hgks_attach_nccl: rank/world out of range");
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof id);
+    ncclComm_t comm = nullptr;
+    NK(N.CommInitRank(&comm, world, id, rank));
+    s->comm = comm;
+    s->own_comm = true;
+    return attach_common(s, rank, world);
+}
+
+int hgks_attach_nccl_comm(hgks_solver* s, void* comm, int rank, int world) {
+    GUARD(s);
+    const NcclApi& N = nccl();
+    if (!N.ok) return fail(s, HGKS_ERR_CUDA, "NCCL unavailable: " + N.why);
+    if (!comm) return fail(s, HGKS_ERR_CONFIG, "hgks_attach_nccl_comm: null communicator");
+    if (world < 1 || rank < 0 || rank >= world)
+        return fail(s, HGKS_ERR_CONFIG, "hgks_attach_nccl_comm: rank/world out of range");
+    s->comm = (ncclComm_t)comm;
+    s->own_comm = false;
+    return attach_common(s, rank, world);
+}
+
+int hgks_slab_reduce_sum(hgks_solver* s, double* vals, int n) {
+    GUARD(s);
+    if (n <= 0 || n > 4096) return fail(s, HGKS_ERR_CONFIG, "hgks_slab_reduce_sum: 1..4096 values");
+    if (s->nccl_on()) {
+        CK(cudaMemcpyAsync(s->d_red, vals, n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+        const int rc = nccl_reduce(s, s->d_red, n, false);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(vals, s->d_red, n * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+    } else if (s->host_hooks() && s->hreduce) {
+        if (s->hreduce(s->hreduce_user, HGKS_REDUCE_SUM_F64, vals, n) != 0)
+            return fail(s, HGKS_ERR_CUDA, "host reduce callback failed");
+    }
+    return HGKS_OK;
 }
 
 int hgks_set_stream(hgks_solver* s, void* stream) {
+    GUARD(s);
+    drop_graphs(s);
     if (s->own_stream && s->stream) {
         CK(cudaStreamSynchronize(s->stream));
         cudaStreamDestroy(s->stream);
@@ -947,6 +1420,7 @@ int hgks_set_stream(hgks_solver* s, void* stream) {
 void* hgks_get_stream(hgks_solver* s) { return (void*)s->stream; }
 
 int hgks_synchronize(hgks_solver* s) {
+    GUARD(s);
     CK(cudaStreamSynchronize(s->stream));
     return HGKS_OK;
 }
@@ -962,9 +1436,19 @@ int hgks_kernel_times(hgks_solver* s, double* face_ms, double* cell_ms, double* 
     return HGKS_OK;
 }
 
+void hgks_set_graphs(hgks_solver* s, int on) {
+    if (!on) drop_graphs(s);
+    s->use_graphs = on != 0;
+}
+
+void hgks_set_grid_cap(hgks_solver* s, int ctas) {
+    drop_graphs(s);
+    s->grid_cap = ctas > 0 ? ctas : 0;
+}
+
 int hgks_measure_fp64_peak(int device, double ms, double* tflops) {
     hgks_solver* s = nullptr;  // for CK
-    CK(cudaSetDevice(device));
+    DevGuard g(device);
     const int blocks = 148 * 8, threads = 256;
     double* out = nullptr;
     CK(cudaMalloc(&out, (size_t)blocks * threads * sizeof(double)));

@@ -13,6 +13,13 @@
 namespace hgks_dev {
 namespace {
 
+// persistent grid size: resident CTAs on the GPU, optionally capped
+// (KParams::grid_cap, a test hook that makes every CTA walk many tiles)
+inline int capped(const KParams& kp, int g) {
+    g = std::max(1, g);
+    return kp.grid_cap > 0 ? std::min(g, kp.grid_cap) : g;
+}
+
 template <int P, int DIM, bool VISC>
 struct Launch {
     using SH = Shape<P, DIM>;
@@ -45,7 +52,7 @@ struct Launch {
         const int ntx = (kp.nx + 31) / 32;
         const int ntiles = ntx * kp.ny * layers;
         int first = 0, count = ntiles;
-        int grid = std::min(ntiles, std::max(1, face_grid[AXIS]));
+        int grid = std::min(ntiles, capped(kp, face_grid[AXIS]));
         if (report) {  // the failing face's tile only
             first = t[0] + ntx * (t[1] + kp.ny * t[2]);
             count = 1;
@@ -60,7 +67,7 @@ struct Launch {
         const int ntx = (kp.nx + 31) / 32;
         const int first = ntx * kp.ny * kb, count = ntx * kp.ny * (ke - kb);
         if (count <= 0) return;
-        const int grid = std::min(count, std::max(1, face_grid[AXIS]));
+        const int grid = std::min(count, capped(kp, face_grid[AXIS]));
         face_kernel<P, DIM, VISC, AXIS><<<grid, FaceCTA<P, DIM, AXIS>::NT, face_smem<AXIS>(), st>>>(
             kp, q, f, first, count, 0);
     }
@@ -82,7 +89,7 @@ struct Launch {
         const int ntx = (kp.nx + SH::TC - 1) / SH::TC;
         const int first = ntx * kp.ny * kb, count = ntx * kp.ny * (ke - kb);
         if (count <= 0) return;
-        const int grid = std::min(count, std::max(1, cell_grid[mode]));
+        const int grid = std::min(count, capped(kp, cell_grid[mode]));
         if (mode == MODE_STAGE1)
             cell_kernel<P, DIM, VISC, MODE_STAGE1><<<grid, CellTile<P, DIM, MODE_STAGE1>::NT,
                                                      cell_smem<MODE_STAGE1>(), st>>>(
@@ -105,7 +112,7 @@ struct Launch {
         const int ntx = (kp.nx + SH::TC - 1) / SH::TC;
         const int ntiles = ntx * kp.ny * kp.nzl;
         int first = 0, count = ntiles;
-        int grid = std::min(ntiles, std::max(1, cell_grid[mode]));
+        int grid = std::min(ntiles, capped(kp, cell_grid[mode]));
         if (report) {  // the failing cell's tile only
             first = tile[0] + ntx * (tile[1] + kp.ny * tile[2]);
             count = 1;

@@ -80,6 +80,8 @@ struct Shape {
     static constexpr int MINB_CELL = P == 3 ? 1 : (HGKS_CELL_TC <= 16 ? 2 : 1);
 };
 
+enum : int { SC_DT = 0, SC_INV_DT = 1, SC_RH = 2, SC_ACTIVE = 3, SC_SLOT = 8 };
+
 struct KParams {
     int nx, ny, nzl;       // local cells (nzl owned z layers)
     int S;                 // nx * ny
@@ -93,9 +95,14 @@ struct KParams {
     int count_fluxes;
     int report;            // re-run in report mode: write err_val for the winning key
     int ft_only;           // face pass of S2O4 stage 2: only Ft is consumed, F is not stored
-    double dt, inv_dt;
+    // step scalars live in device memory (written by set_scalars_kernel or,
+    // in the device-resident advance loop, by dt_finalize_kernel), so a
+    // captured step graph is independent of dt:
+    //   scal[SC_DT] dt, [SC_INV_DT] 1/dt, [SC_RH] dt / (4 mu), [SC_ACTIVE] 0
+    //   = this step is a no-op (the loop halted or reached t_end)
+    const double* scal;
     double two_mu;         // 2 mu: face tau = 2 mu / (p_l + p_r)
-    double rh_coef;        // dt / (4 mu): dt / (2 tau) = (p_l + p_r) rh_coef
+    int grid_cap;          // > 0: cap on the persistent grids (tests: many tiles per CTA)
     GasC gas;
     const double* dx;      // [nx] widths
     const double* dy;      // [ny]
@@ -353,6 +360,8 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
     constexpr int STG = 2 * NC * 32;  // one stage: [side][comp][32]
     extern __shared__ double smem[];
 
+    if (kp.scal[SC_ACTIVE] == 0.0) return;  // halted device loop: no-op step
+    const double inv_dt = kp.scal[SC_INV_DT], rh_coef = kp.scal[SC_RH];
     const int tid = threadIdx.x;
     const int nx = kp.nx, ny = kp.ny;
     const int ntx = (nx + 31) / 32;
@@ -444,7 +453,7 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
             {
                 // tau = mu / mean trace pressure (dg.hpp:378-383); dt/(2 tau) without a division
                 const double tau = VISC ? kp.two_mu / psum : 0.0;
-                const TimeW tw = time_weights_r(tau, kp.inv_dt, VISC ? psum * kp.rh_coef : 0.0);
+                const TimeW tw = time_weights_r(tau, inv_dt, VISC ? psum * rh_coef : 0.0);
                 rcs[2] = flux_merge<VISC>(kp.gas, tw, acc, F, Ft, bads[2]);
             }
             if (rcs[0] | rcs[1] | rcs[2]) {
@@ -473,7 +482,7 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
             if (!fail) {
                 // tau = mu / mean trace pressure (dg.hpp:378-383); dt/(2 tau) without a division
                 const double tau = VISC ? kp.two_mu / psum : 0.0;
-                const TimeW tw = time_weights_r(tau, kp.inv_dt, VISC ? psum * kp.rh_coef : 0.0);
+                const TimeW tw = time_weights_r(tau, inv_dt, VISC ? psum * rh_coef : 0.0);
                 double bad = 0.0;
                 const int rc = flux_merge<VISC>(kp.gas, tw, acc, F, Ft, bad);
                 if (rc) {
@@ -771,11 +780,12 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
             }
         }
     };
+    if (kp.scal[SC_ACTIVE] == 0.0) return;  // halted device loop: no-op step
+    const double dt = kp.scal[SC_DT];
     const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
     TI cur = walk.of(t0);
     if (t0 < tile_end) prefetch_coef(cur, coefb, geob);
     cp_async_commit();
-    const double dt = kp.dt;
     int n = 0;
     for (int t = t0; t < tile_end; t += step, ++n) {
         double* sc = coefb + (n & 1) * CT::COEF;

@@ -9,13 +9,23 @@ flux of its top boundary face redundantly from identical inputs, so results
 are bitwise identical for any rank count. dt is a min-allreduce (order
 independent, exact).
 
-Transport is torch.distributed (NCCL on GPUs, gloo on CPU for tests): the
-solver packs its boundary layers into contiguous device buffers
-(hgks_halo_pack), this module moves them, the solver unpacks
-(hgks_halo_unpack). The exchange is split (hgks_set_halo_exchange_split):
-it is enqueued right after the pack, the faces that need no ghost layer run
-while the layers are in flight, and the solver stream waits for the transfer
-only before the unpack and the two boundary z-face layers.
+Two transports:
+
+* NCCL (the product path on B200s): the library owns the data plane
+  (hgks_attach_nccl). Rank 0's NCCL id is broadcast once over
+  torch.distributed; after that the halo send/recv pair, the dt and
+  error-key min-reductions all run inside libhgks_b200.so on device streams,
+  captured in the per-step CUDA graph, with no Python on the step path.
+* torch.distributed callbacks (gloo; the CPU tests and the one-GPU
+  multi-rank test mode): the solver packs its boundary layers into
+  contiguous device buffers (hgks_halo_pack), this module moves them, the
+  solver unpacks (hgks_halo_unpack). The exchange is split
+  (hgks_set_halo_exchange_split): it is enqueued right after the pack, the
+  faces that need no ghost layer run while the layers are in flight, and the
+  solver stream waits for the transfer only before the unpack and the two
+  boundary z-face layers. dt bits, error keys and report values go through
+  the host reduce hook (hgks_set_host_reduce), which every rank joins even
+  when its own cells failed.
 """
 from __future__ import annotations
 
@@ -141,10 +151,51 @@ def sum_allreduce(values, device: Optional[str] = None, group=None):
     return acc
 
 
-def attach(solver, rank: int, world: int, device: int, group=None):
-    """Wire a slab solver to torch.distributed: halo exchange on the solver's
-    stream (which must be torch's current stream) and min-allreduce of dt."""
+def u64_min_allreduce(values, group=None):
+    """In-place min over ranks of a uint64 array (error keys, dt bit patterns):
+    the sign bit is flipped so the order survives the int64 all-reduce."""
+    import numpy as np
     import torch
+    import torch.distributed as dist
+
+    flip = np.uint64(1 << 63)
+    t = torch.from_numpy((values ^ flip).view(np.int64).copy())
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    values[:] = t.numpy().view(np.uint64) ^ flip
+
+
+def host_reduce(op: int, values, group=None):
+    """The solver's host reduce hook over torch.distributed (gloo)."""
+    if op == 0:
+        u64_min_allreduce(values, group=group)
+    else:
+        values[:] = sum_allreduce(values.tolist(), device="cpu", group=group)
+
+
+def attach_nccl(solver, rank: int, world: int, group=None):
+    """In-library NCCL data plane: rank 0 makes the NCCL id, torch.distributed
+    broadcasts it once, every rank attaches (hgks_attach_nccl)."""
+    import torch.distributed as dist
+
+    obj = [solver.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    solver.attach_nccl(obj[0], rank, world)
+
+
+def attach(solver, rank: int, world: int, device: int, group=None, transport: str = "auto"):
+    """Wire a slab solver to its neighbours. transport "nccl" (default on an
+    NCCL process group): the library's own data plane; "torch": halo exchange
+    through torch.distributed callbacks on the solver's stream (which must be
+    torch's current stream) and reductions through the host reduce hook."""
+    import torch
+    import torch.distributed as dist
+
+    backend = dist.get_backend(group)
+    if transport == "auto":
+        transport = "nccl" if backend == "nccl" else "torch"
+    if transport == "nccl":
+        attach_nccl(solver, rank, world, group)
+        return None
 
     nbytes = solver.halo_bytes()
     ptrs = solver.halo_buffers()
@@ -172,10 +223,7 @@ def attach(solver, rank: int, world: int, device: int, group=None):
         if not same:
             ts.synchronize()
 
-    import torch.distributed as dist
-
-    red_dev = "cpu" if dist.get_backend(group) == "gloo" else f"cuda:{device}"
     # interior faces run while the layers are in flight
     solver.set_halo_exchange_split(start, finish)
-    solver.set_dt_reduce(lambda v: min_allreduce(v, device=red_dev, group=group))
+    solver.set_host_reduce(lambda op, vals: host_reduce(op, vals, group=group))
     return views

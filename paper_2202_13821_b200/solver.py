@@ -250,6 +250,8 @@ class Solver:
         ncell_owned = self.ncoeffs // (5 * self.N)
         fb = [np.empty(ncell_owned * self.face_points(a) * 10) for a in range(3)] if faces else [None] * 3
         c = None if coeffs is None else np.ascontiguousarray(coeffs, dtype=np.float64).ravel()
+        if c is not None and c.size != self.ncoeffs:
+            raise ConfigError(f"coeffs has {c.size} values, expected {self.ncoeffs}")
         self._check(self.L.hgks_residual(self.h, _ptr(c), dt, _ptr(R), _ptr(Rt), *(_ptr(f) for f in fb)))
         out = {"R": R, "Rt": Rt}
         if faces:
@@ -258,6 +260,8 @@ class Solver:
 
     def apply_inverse_mass(self, R):
         R = np.ascontiguousarray(R, dtype=np.float64).ravel()
+        if R.size != self.ncoeffs:
+            raise ConfigError(f"R has {R.size} values, expected {self.ncoeffs}")
         L = np.empty_like(R)
         self._check(self.L.hgks_apply_inverse_mass(self.h, _ptr(R), _ptr(L)))
         return L
@@ -287,6 +291,31 @@ class Solver:
     def advance_to(self, t_end: float, cfl: float, dt_fixed: float = 0.0, record_interval: float = 0.0) -> int:
         n = ctypes.c_int()
         self._check(self.L.hgks_advance(self.h, t_end, cfl, dt_fixed, record_interval, ctypes.byref(n)))
+        return n.value
+
+    def advance_records(self, t_end: float, cfl: float, dt_fixed: float = 0.0, record_interval: float = 0.0,
+                        first_record: float = 0.0, max_steps: int = 0,
+                        on_record: Optional[Callable[[float], None]] = None) -> int:
+        """hgks_advance_records: the device-resident loop (dt, clipping, commit
+        and failure checks on the GPU, one CUDA graph per step);
+        on_record(t) runs after each step that lands on a record time, with
+        the solver showing that step's state."""
+        n = ctypes.c_int()
+        err = []
+
+        def cb(user, h, t):
+            try:
+                on_record(t)
+                return 0
+            except Exception as e:  # noqa: BLE001 — re-raised below
+                err.append(e)
+                return 1
+        c = _lib.RECORD_FN(cb) if on_record is not None else _lib.RECORD_FN()
+        rc = self.L.hgks_advance_records(self.h, t_end, cfl, dt_fixed, record_interval, first_record,
+                                         max_steps, c, None, ctypes.byref(n))
+        if err:
+            raise err[0]
+        self._check(rc)
         return n.value
 
     # -- cases, diagnostics
@@ -390,18 +419,48 @@ class Solver:
         self._cbs += [a, b]
         self.L.hgks_set_halo_exchange_split(self.h, a, b, None)
 
-    def set_dt_reduce(self, fn: Callable[[float], float]):
-        def cb(user, val):
+    def set_host_reduce(self, fn: Callable[[int, np.ndarray], None]):
+        """fn(op, values) reduces `values` in place over the slabs: op 0 = min
+        of uint64 (error keys, dt bits), op 1 = sum of float64."""
+        def cb(user, op, ptr, n):
             try:
-                val[0] = fn(val[0])
+                ct = ctypes.c_uint64 if op == _lib.HGKS_REDUCE_MIN_U64 else ctypes.c_double
+                arr = np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ct)), shape=(n,))
+                fn(op, arr)
                 return 0
-            except Exception:  # noqa: BLE001
+            except Exception:  # noqa: BLE001 — reported as an ABI failure
                 import traceback
                 traceback.print_exc()
                 return 1
-        c = _lib.MIN_FN(cb)
+        c = _lib.REDUCE_FN(cb)
         self._cbs.append(c)
-        self.L.hgks_set_dt_reduce(self.h, c, None)
+        self.L.hgks_set_host_reduce(self.h, c, None)
+
+    # -- in-library NCCL data plane
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        rc = _lib.load().hgks_nccl_unique_id(buf, 128)
+        if rc != 0:
+            raise CudaError("ncclGetUniqueId failed (libnccl.so.2 not loadable?)")
+        return buf.raw
+
+    def attach_nccl(self, unique_id: bytes, rank: int, world: int):
+        """Join the z-slab ring: halos, dt and error keys over NCCL inside the
+        library (no Python on the step path)."""
+        self._check(self.L.hgks_attach_nccl(self.h, unique_id, rank, world))
+
+    def slab_reduce_sum(self, values):
+        v = np.ascontiguousarray(values, dtype=np.float64).copy()
+        self._check(self.L.hgks_slab_reduce_sum(self.h, _ptr(v), v.size))
+        return v
+
+    def set_graphs(self, on: bool = True):
+        self.L.hgks_set_graphs(self.h, int(on))
+
+    def set_grid_cap(self, ctas: int):
+        """Test hook: cap the persistent grids (every CTA walks many tiles)."""
+        self.L.hgks_set_grid_cap(self.h, int(ctas))
 
 
 def measure_fp64_peak(device: int = 0, ms: float = 50.0) -> float:
@@ -522,15 +581,12 @@ def advance(r: RunResult, cfg: CaseConfig, opt: RunOptions, on_record: Callable[
     next_record = opt.record_interval
     on_record(r)
     dt_fixed = opt.dt_fixed if opt.dt_fixed is not None else 0.0
-    # the device loop (hgks_advance) runs each record interval: dt = compute_dt
-    # (or dt_fixed) clipped to the chunk end, which is min(t_end, next record)
-    # exactly as solver.hpp:91-93 clips; " at t=<t>" is appended on failure
-    while r.solver.time < t_end - 1e-14 * t_end:
-        chunk_end = min(t_end, next_record) if record else t_end
-        r.steps += r.solver.advance_to(chunk_end, cfl, dt_fixed, 0.0)
-        if record and r.solver.time >= next_record - 1e-12:
-            on_record(r)
-            next_record += opt.record_interval
+    # the device-resident loop (hgks_advance_records): dt = compute_dt (or
+    # dt_fixed) clipped to t_end and, for tgv, to the next record, exactly as
+    # solver.hpp:91-93; on_record runs at each record time; " at t=<t>" is
+    # appended to state errors
+    r.steps += r.solver.advance_records(t_end, cfl, dt_fixed, opt.record_interval if record else 0.0,
+                                        next_record, 0, (lambda t: on_record(r)) if record else None)
 
 
 def dissipation_from_series(ek, dt):

@@ -49,32 +49,23 @@ def test_restatement_matches_golden(oracle_mod, path):
                                                ("adv2d", 6, 2, True)])
 def test_restatement_bitwise_vs_reference(oracle_mod, case, n, deg, nonuni):
     O = oracle_mod
-    so = os.path.join(os.path.dirname(O.REF_SO), "libhgks_ref_nofma.so")
-    if not os.path.exists(so):
+    if not os.path.exists(O.REF_NOFMA_SO):
         pytest.skip("reference build (contraction off) not available")
-    L = O._ref_lib()  # make sure argtypes exist on the stock build; load the nofma one separately
-    import ctypes
-    saved = (O._ref, O.REF_SO)
-    try:
-        O._ref, O.REF_SO = None, so
-        r = O.RefRun(case, n, deg, nonuniform=nonuni, workers=3)
-        o = O.Oracle(case, n, deg, nonuniform=nonuni)
-        q0, _ = r.get_state()
-        assert np.array_equal(o.state, q0)
-        cfl = 0.15 if deg == 2 else 0.09
-        for _ in range(3):
-            dt = r.compute_dt(cfl)
-            assert dt == o.compute_dt(cfl)
-            a, b = r.residual(dt, faces=True), o.residual(dt, faces=True)
-            assert np.array_equal(a["R"], b["R"]) and np.array_equal(a["Rt"], b["Rt"])
-            for x, y in zip(a["faces"], b["faces"]):
-                assert np.array_equal(x, y)
-            r.step(dt)
-            o.step(dt)
-        assert np.array_equal(r.get_state()[0], o.state)
-    finally:
-        O._ref, O.REF_SO = saved
-    del L, ctypes
+    r = O.RefRun(case, n, deg, nonuniform=nonuni, workers=3, lib="nofma")
+    o = O.Oracle(case, n, deg, nonuniform=nonuni)
+    q0, _ = r.get_state()
+    assert np.array_equal(o.state, q0)
+    cfl = 0.15 if deg == 2 else 0.09
+    for _ in range(3):
+        dt = r.compute_dt(cfl)
+        assert dt == o.compute_dt(cfl)
+        a, b = r.residual(dt, faces=True), o.residual(dt, faces=True)
+        assert np.array_equal(a["R"], b["R"]) and np.array_equal(a["Rt"], b["Rt"])
+        for x, y in zip(a["faces"], b["faces"]):
+            assert np.array_equal(x, y)
+        r.step(dt)
+        o.step(dt)
+    assert np.array_equal(r.get_state()[0], o.state)
 
 
 def test_compute_dt_rest_gas_known_answer(oracle_mod):
