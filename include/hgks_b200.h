@@ -143,6 +143,18 @@ int hgks_tgv_diagnostics(hgks_solver* s, double* ek_vol, double* ens_vol, double
  * sqrt(out1), sqrt(out2)} after summing over slabs). */
 int hgks_error_norms(hgks_solver* s, const char* case_name, double t, double* out);
 
+/* project(field, mesh, tab, part) (dg.hpp:193-220) for a caller-supplied
+ * field: samples[(cell*npts + p)*5 + var] are the field's conserved values at
+ * the projection points of the owned cells, x = center + h/2 * ref_p with the
+ * (k+2)^dim Gauss points in the reference's order (dg.hpp:102-105); the
+ * weighted sums run on the device. npts = hgks_projection_npts. */
+int hgks_projection_npts(const hgks_solver* s);
+int hgks_project_samples(hgks_solver* s, const double* samples, double t);
+/* error_norms(state, mesh, tab, exact, part) (dg.hpp:228-266) for a
+ * caller-supplied exact field: rho_exact[cell*npts + p] at the projection
+ * points; out as hgks_error_norms (unreduced sums). */
+int hgks_error_norms_samples(hgks_solver* s, const double* rho_exact, double* out);
+
 /* ---- multi-GPU z-slabs. The halo is one layer of cell
  * coefficients below and above the owned slab, packed contiguously:
  * [comp][cell-in-layer], hgks_halo_bytes() per direction. */

@@ -1,0 +1,5 @@
+// Drop-in for the reference's proj/include/hgks/basis.hpp (BasisSet): with
+// -I include/hgks_b200/compat -I include, a reference caller's
+// #include "hgks/basis.hpp" resolves here and gets the B200-backed API.
+#pragma once
+#include "hgks_b200/hgks.hpp"

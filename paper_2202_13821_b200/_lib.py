@@ -27,7 +27,8 @@ EXPORTS = [
     "hgks_residual", "hgks_apply_inverse_mass", "hgks_compute_dt", "hgks_step",
     "hgks_two_stage_step_host", "hgks_two_stage_step_host_streamed", "hgks_advance_records", "hgks_advance",
     "hgks_set_count_fluxes", "hgks_flux_evaluations",
-    "hgks_project_case", "hgks_tgv_diagnostics", "hgks_error_norms", "hgks_halo_bytes", "hgks_halo_buffers",
+    "hgks_project_case", "hgks_tgv_diagnostics", "hgks_error_norms", "hgks_projection_npts",
+    "hgks_project_samples", "hgks_error_norms_samples", "hgks_halo_bytes", "hgks_halo_buffers",
     "hgks_halo_pack", "hgks_halo_unpack", "hgks_set_halo_exchange", "hgks_set_halo_exchange_split", "hgks_step_phase",
     "hgks_set_host_reduce", "hgks_nccl_unique_id", "hgks_attach_nccl", "hgks_attach_nccl_comm",
     "hgks_slab_reduce_sum", "hgks_set_stream", "hgks_get_stream", "hgks_synchronize",
@@ -96,6 +97,9 @@ def load():
     L.hgks_project_case.argtypes = [sp, ctypes.c_char_p, ctypes.c_double]
     L.hgks_tgv_diagnostics.argtypes = [sp, _dp, _dp, _dp]
     L.hgks_error_norms.argtypes = [sp, ctypes.c_char_p, ctypes.c_double, _dp]
+    L.hgks_projection_npts.argtypes = [sp]
+    L.hgks_project_samples.argtypes = [sp, _dp, ctypes.c_double]
+    L.hgks_error_norms_samples.argtypes = [sp, _dp, _dp]
     L.hgks_halo_bytes.argtypes = [sp]
     L.hgks_halo_bytes.restype = ctypes.c_long
     L.hgks_halo_buffers.argtypes = [sp, _u64p, _u64p, _u64p, _u64p]

@@ -42,7 +42,9 @@ def _nvcc():
 
 
 def _sources():
-    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INC, "hgks_b200.h")]
+    return ([os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INC, "hgks_b200.h")] +
+            [os.path.join(INC, "hgks_b200", f) for f in os.listdir(os.path.join(INC, "hgks_b200"))
+             if f.endswith(".h")])
 
 
 def up_to_date() -> bool:

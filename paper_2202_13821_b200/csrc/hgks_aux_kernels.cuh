@@ -323,10 +323,14 @@ __device__ __forceinline__ void case_field(const CaseParams& c, const double* x,
 template <int NC>
 __global__ void __launch_bounds__(128) project_kernel(KParams kp, CaseParams cp,
                                                       const double* __restrict__ ctr,
-                                                      double* __restrict__ q, long ncell) {
+                                                      double* __restrict__ q, long ncell,
+                                                      const double* __restrict__ samples, long c0) {
+    // samples (optional): the field at the projection points of cells
+    // [c0, c0 + ncell), [(cell - c0) * npts + p][5], evaluated by the caller
+    // (a host-side field function, dg.hpp:193); else the named case's field
     constexpr int N = NC / 5;
-    const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (c >= ncell) return;
+    const long c = c0 + blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (c >= c0 + ncell) return;
     const int i = (int)(c % kp.nx), j = (int)((c / kp.nx) % kp.ny), k = (int)(c / kp.S);
     const double h[3] = {kp.dx[i], kp.dy[j], kp.dz[k + 1]};
     const double x0[3] = {ctr[i], ctr[kp.nx + j], ctr[kp.nx + kp.ny + k]};
@@ -337,7 +341,12 @@ __global__ void __launch_bounds__(128) project_kernel(KParams kp, CaseParams cp,
         const double* r = kp.tab + kp.off_pref + 3 * p;
         const double x[3] = {x0[0] + 0.5 * h[0] * r[0], x0[1] + 0.5 * h[1] * r[1], x0[2] + 0.5 * h[2] * r[2]};
         double f[5];
-        case_field(cp, x, f);
+        if (samples) {
+#pragma unroll
+            for (int v = 0; v < 5; ++v) f[v] = samples[((c - c0) * cp.npts + p) * 5 + v];
+        } else {
+            case_field(cp, x, f);
+        }
         const double wq = kp.tab[kp.off_pw + p];
         const double* B = kp.tab + kp.off_pB + p * N;
 #pragma unroll
@@ -426,13 +435,14 @@ __global__ void __launch_bounds__(256) tgv_kernel(KParams kp, int npts,
 }
 
 inline void launch_project(int degree, int dim, const KParams& kp, const CaseParams& cp,
-                           const double* ctr, double* q, long ncell, cudaStream_t st) {
+                           const double* ctr, double* q, long ncell, cudaStream_t st,
+                           const double* samples = nullptr, long c0 = 0) {
     const int blocks = (int)((ncell + 127) / 128);
     const int NC = 5 * (dim == 3 ? (degree == 1 ? 4 : degree == 2 ? 10 : 20) : (degree == 2 ? 6 : 10));
-    if (NC == 20) project_kernel<20><<<blocks, 128, 0, st>>>(kp, cp, ctr, q, ncell);
-    else if (NC == 30) project_kernel<30><<<blocks, 128, 0, st>>>(kp, cp, ctr, q, ncell);
-    else if (NC == 50) project_kernel<50><<<blocks, 128, 0, st>>>(kp, cp, ctr, q, ncell);
-    else project_kernel<100><<<blocks, 128, 0, st>>>(kp, cp, ctr, q, ncell);
+    if (NC == 20) project_kernel<20><<<blocks, 128, 0, st>>>(kp, cp, ctr, q, ncell, samples, c0);
+    else if (NC == 30) project_kernel<30><<<blocks, 128, 0, st>>>(kp, cp, ctr, q, ncell, samples, c0);
+    else if (NC == 50) project_kernel<50><<<blocks, 128, 0, st>>>(kp, cp, ctr, q, ncell, samples, c0);
+    else project_kernel<100><<<blocks, 128, 0, st>>>(kp, cp, ctr, q, ncell, samples, c0);
 }
 
 inline void launch_tgv(int degree, int dim, const KParams& kp, int npts, const double* q, long ncell,
@@ -450,7 +460,10 @@ inline void launch_tgv(int degree, int dim, const KParams& kp, int npts, const d
 template <int N>
 __global__ void __launch_bounds__(256) error_kernel(KParams kp, CaseParams cp, const double* __restrict__ ctr,
                                                     const double* __restrict__ q, long ncell,
-                                                    double* __restrict__ part) {
+                                                    double* __restrict__ part,
+                                                    const double* __restrict__ rho_samples) {
+    // rho_samples (optional): the exact density at the projection points,
+    // [cell * npts + p], evaluated by the caller (dg.hpp:228 takes a function)
     __shared__ double red[3][256];
     double s1 = 0, s2 = 0, sc = 0;
     for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < ncell; c += (long)gridDim.x * blockDim.x) {
@@ -466,7 +479,8 @@ __global__ void __launch_bounds__(256) error_kernel(KParams kp, CaseParams cp, c
             const double* r = kp.tab + kp.off_pref + 3 * p;
             const double x[3] = {x0[0] + 0.5 * h[0] * r[0], x0[1] + 0.5 * h[1] * r[1], x0[2] + 0.5 * h[2] * r[2]};
             double f[5];
-            case_field(cp, x, f);
+            if (rho_samples) f[0] = rho_samples[c * cp.npts + p];
+            else case_field(cp, x, f);
             const double* B = kp.tab + kp.off_pB + p * N;
             double rh = 0;
 #pragma unroll
@@ -497,12 +511,13 @@ __global__ void __launch_bounds__(256) error_kernel(KParams kp, CaseParams cp, c
 }
 
 inline void launch_error(int degree, int dim, const KParams& kp, const CaseParams& cp, const double* ctr,
-                         const double* q, long ncell, double* part, int blocks, cudaStream_t st) {
+                         const double* q, long ncell, double* part, int blocks, cudaStream_t st,
+                         const double* rho_samples = nullptr) {
     const int N = dim == 3 ? (degree == 1 ? 4 : degree == 2 ? 10 : 20) : (degree == 2 ? 6 : 10);
-    if (N == 4) error_kernel<4><<<blocks, 256, 0, st>>>(kp, cp, ctr, q, ncell, part);
-    else if (N == 6) error_kernel<6><<<blocks, 256, 0, st>>>(kp, cp, ctr, q, ncell, part);
-    else if (N == 10) error_kernel<10><<<blocks, 256, 0, st>>>(kp, cp, ctr, q, ncell, part);
-    else error_kernel<20><<<blocks, 256, 0, st>>>(kp, cp, ctr, q, ncell, part);
+    if (N == 4) error_kernel<4><<<blocks, 256, 0, st>>>(kp, cp, ctr, q, ncell, part, rho_samples);
+    else if (N == 6) error_kernel<6><<<blocks, 256, 0, st>>>(kp, cp, ctr, q, ncell, part, rho_samples);
+    else if (N == 10) error_kernel<10><<<blocks, 256, 0, st>>>(kp, cp, ctr, q, ncell, part, rho_samples);
+    else error_kernel<20><<<blocks, 256, 0, st>>>(kp, cp, ctr, q, ncell, part, rho_samples);
 }
 
 }  // namespace hgks_dev

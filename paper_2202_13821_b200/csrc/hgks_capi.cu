@@ -16,7 +16,7 @@
 #include <vector>
 
 #include "../../include/hgks_b200.h"
-#include "hgks_basis.h"
+#include "../../include/hgks_b200/basis_tables.h"
 #include "hgks_aux_kernels.cuh"
 #include "hgks_kernels.cuh"
 #include "hgks_launch.h"
@@ -1195,7 +1195,8 @@ namespace {
 // the owned cells on the device; caller frees *d_ctr
 int case_setup(hgks_solver* s, const char* case_name, double t, CaseParams& cp, double** d_ctr) {
     int cid;
-    if (!std::strcmp(case_name, "adv2d")) cid = CASE_ADV2D;
+    if (!case_name) cid = CASE_ADV3D;  // caller-sampled field: the case formulas are unused
+    else if (!std::strcmp(case_name, "adv2d")) cid = CASE_ADV2D;
     else if (!std::strcmp(case_name, "adv3d")) cid = CASE_ADV3D;
     else if (!std::strcmp(case_name, "vortex2d")) cid = CASE_VORTEX2D;
     else if (!std::strcmp(case_name, "tgv")) cid = CASE_TGV;
@@ -1284,6 +1285,69 @@ int hgks_tgv_diagnostics(hgks_solver* s, double* ek_vol, double* ens_vol, double
     if (ek_vol) *ek_vol = e;
     if (ens_vol) *ens_vol = z;
     if (volume) *volume = v;
+    return HGKS_OK;
+}
+
+int hgks_projection_npts(const hgks_solver* s) { return s->tabs.proj.npts; }
+
+int hgks_project_samples(hgks_solver* s, const double* samples, double t) {
+    GUARD(s);
+    CaseParams cp;
+    double* d_ctr = nullptr;
+    int rc = case_setup(s, nullptr, t, cp, &d_ctr);
+    if (rc) return rc;
+    KParams kp = make_params(s, 0, 0);
+    const long ncell = s->S * s->nzl;
+    const long per = (long)cp.npts * 5;
+    // staged in bounded chunks of cells (the samples are 5 * npts doubles per cell)
+    const long chunk = std::max(1L, std::min(ncell, (256L << 20) / (per * 8)));
+    double* d_smp = nullptr;
+    CK(cudaMalloc(&d_smp, (size_t)chunk * per * sizeof(double)));
+    for (long c0 = 0; c0 < ncell; c0 += chunk) {
+        const long n = std::min(chunk, ncell - c0);
+        CK(cudaMemcpyAsync(d_smp, samples + c0 * per, (size_t)n * per * sizeof(double), cudaMemcpyHostToDevice,
+                           s->stream));
+        launch_project(s->cfg.degree, s->cfg.dim, kp, cp, d_ctr, s->qa(), n, s->stream, d_smp, c0);
+        ++s->launches;
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s->stream));
+    }
+    cudaFree(d_smp);
+    cudaFree(d_ctr);
+    s->time = t;
+    return HGKS_OK;
+}
+
+int hgks_error_norms_samples(hgks_solver* s, const double* rho_exact, double* out) {
+    GUARD(s);
+    CaseParams cp;
+    double* d_ctr = nullptr;
+    int rc = case_setup(s, nullptr, 0.0, cp, &d_ctr);
+    if (rc) return rc;
+    const long ncell = s->S * s->nzl;
+    double* d_rho = nullptr;
+    CK(cudaMalloc(&d_rho, (size_t)ncell * cp.npts * sizeof(double)));
+    CK(cudaMemcpyAsync(d_rho, rho_exact, (size_t)ncell * cp.npts * sizeof(double), cudaMemcpyHostToDevice,
+                       s->stream));
+    KParams kp = make_params(s, 0, 0);
+    const int blocks = 148 * 2;
+    launch_error(s->cfg.degree, s->cfg.dim, kp, cp, d_ctr, s->qa(), ncell, s->d_red, blocks, s->stream, d_rho);
+    ++s->launches;
+    CK(cudaGetLastError());
+    std::vector<double> part(3 * blocks);
+    CK(cudaMemcpyAsync(part.data(), s->d_red, part.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    cudaFree(d_rho);
+    cudaFree(d_ctr);
+    double l1 = 0, l2 = 0, ec = 0;
+    for (int b = 0; b < blocks; ++b) {  // fixed order
+        l1 += part[3 * b];
+        l2 += part[3 * b + 1];
+        ec += part[3 * b + 2];
+    }
+    out[0] = l1;
+    out[1] = l2;
+    out[2] = ec;
     return HGKS_OK;
 }
 

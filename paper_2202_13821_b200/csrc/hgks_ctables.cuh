@@ -1,4 +1,4 @@
-// Compile-time basis / quadrature tables (the same values hgks_basis.h
+// Compile-time basis / quadrature tables (the same values include/hgks_b200/basis_tables.h
 // tabulates on the host: graded tensor-Legendre basis, basis.hpp:64-82;
 // Gauss-Legendre points, quadrature.hpp:15-58; point order of DGTables::make,
 // dg.hpp:91-128). They are built once per (degree, dim) by the front end's

@@ -110,7 +110,7 @@ struct KParams {
     const double* i2dx;    // 2 / h per axis (same indexing)
     const double* i2dy;
     const double* i2dz;
-    const double* tab;     // runtime table image (aux kernels; hgks_basis.h)
+    const double* tab;     // runtime table image (aux kernels; include/hgks_b200/basis_tables.h)
     long off_fB[3][2], off_fdB[3][2], off_fw[3];
     long off_vB, off_vdB, off_vw, off_pB, off_pdB, off_pw, off_pref, off_massf;
     unsigned long long* err_key;
