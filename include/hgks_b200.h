@@ -82,6 +82,10 @@ int hgks_apply_inverse_mass(hgks_solver* s, const double* R, double* L);
 /* compute_dt(state, mesh, gas, ctrl, degree) (integrator.hpp:27-45) on the
  * current state, ctrl.cfl = cfl. */
 int hgks_compute_dt(hgks_solver* s, double cfl, double* dt);
+/* the same with the degree of the viscous bound given explicitly (the
+ * reference's compute_dt takes it as an argument, independent of the state's
+ * basis: integrator.hpp:27, :40) */
+int hgks_compute_dt_k(hgks_solver* s, double cfl, int degree, double* dt);
 
 /* two_stage_step(q, dt, eval, scratch) (integrator.hpp:64-75) with the eval
  * of solver.hpp:81-88 (residual + inverse mass, the same full dt in both
@@ -231,6 +235,10 @@ void hgks_set_graphs(hgks_solver* s, int on);
 /* test hook: cap the persistent face / cell grids at `ctas` CTAs (0 = the
  * resident count), so every CTA walks many tiles even on small meshes */
 void hgks_set_grid_cap(hgks_solver* s, int ctas);
+/* test hook: seed != 0 makes every warp of the persistent kernels sleep a
+ * pseudo-random 0..4 us before each cp.async wait and barrier (a race
+ * shaker: results must stay bitwise identical); 0 = off */
+void hgks_set_race_shake(hgks_solver* s, unsigned seed);
 
 /* Roofline denominator: sustained FP64 FMA throughput of `device`, measured
  * with a DFMA-chain kernel over ~`ms` milliseconds (CUDA events). Writes

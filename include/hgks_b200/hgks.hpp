@@ -290,21 +290,26 @@ struct StepControl {
 
 inline double default_cfl(int degree) { return degree == 2 ? 0.15 : 0.09; }
 
-namespace detail {
-inline int dim_of(const DGState& s, int degree) {
-    const int n3 = degree == 1 ? 4 : degree == 2 ? 10 : 20;
-    return s.N == n3 ? 3 : 2;
-}
-}  // namespace detail
-
-/// compute_dt (integrator.hpp:27-45) from the cell means, on the GPU.
+/// compute_dt (integrator.hpp:27-45) from the cell means, on the GPU. Only
+/// the means enter, and `degree` only through the viscous bound, so the means
+/// of any state are evaluated on the mesh's P2 device solver.
 inline double compute_dt(const DGState& s, const Mesh& mesh, const GasModel& gas, const StepControl& ctrl,
                          int degree) {
     if (ctrl.dt_fixed) return *ctrl.dt_fixed;
-    auto d = detail::Registry::get().acquire(mesh, degree, detail::dim_of(s, degree), gas, 0);
-    d->upload(s);
+    const int dim = mesh.nz > 1 ? 3 : 2;
+    const int N = dim == 3 ? 10 : 6;
+    auto d = detail::Registry::get().acquire(mesh, 2, dim, gas, 0);
+    if (s.N == N) {
+        d->upload(s);
+    } else {
+        DGState m = DGState::zeros(mesh.ncells(), N);
+        for (int c = 0; c < mesh.ncells(); ++c)
+            for (int v = 0; v < 5; ++v) m.coeff(c, 0, v) = s.coeff(c, 0, v);
+        m.time = s.time;
+        d->upload(m);
+    }
     double dt = 0.0;
-    d->check(hgks_compute_dt(d->s, ctrl.cfl, &dt));
+    d->check(hgks_compute_dt_k(d->s, ctrl.cfl, degree, &dt));
     return dt;
 }
 
@@ -641,8 +646,8 @@ inline RunResult run_case(const CaseConfig& cfg, const RunOptions& opt) {
     auto d = detail::device_for(r.mesh, r.scheme);
     const bool tgv = cfg.name == "tgv";
     // records straight from the device state (no download per record)
-    if (tgv) r.records.push_back(detail::tgv_record(d->s, r.scheme.gas.mu_ref, r.state.time));
     d->upload(r.state);
+    if (tgv) r.records.push_back(detail::tgv_record(d->s, r.scheme.gas.mu_ref, r.state.time));
     detail::advance_on_device(r, cfg, opt, *d, [&](double t) {
         r.records.push_back(detail::tgv_record(d->s, r.scheme.gas.mu_ref, t));
     });

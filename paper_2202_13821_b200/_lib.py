@@ -24,7 +24,7 @@ _u64p = ctypes.POINTER(ctypes.c_ulonglong)
 EXPORTS = [
     "hgks_abi_version", "hgks_create", "hgks_destroy", "hgks_last_error", "hgks_error_info",
     "hgks_num_basis", "hgks_num_coeffs", "hgks_face_points", "hgks_set_state", "hgks_get_state",
-    "hgks_residual", "hgks_apply_inverse_mass", "hgks_compute_dt", "hgks_step",
+    "hgks_residual", "hgks_apply_inverse_mass", "hgks_compute_dt", "hgks_compute_dt_k", "hgks_step",
     "hgks_two_stage_step_host", "hgks_two_stage_step_host_streamed", "hgks_advance_records", "hgks_advance",
     "hgks_set_count_fluxes", "hgks_flux_evaluations",
     "hgks_project_case", "hgks_tgv_diagnostics", "hgks_error_norms", "hgks_projection_npts",
@@ -32,7 +32,7 @@ EXPORTS = [
     "hgks_halo_pack", "hgks_halo_unpack", "hgks_set_halo_exchange", "hgks_set_halo_exchange_split", "hgks_step_phase",
     "hgks_set_host_reduce", "hgks_nccl_unique_id", "hgks_attach_nccl", "hgks_attach_nccl_comm",
     "hgks_slab_reduce_sum", "hgks_set_stream", "hgks_get_stream", "hgks_synchronize",
-    "hgks_launch_count", "hgks_set_kernel_timing", "hgks_kernel_times", "hgks_set_graphs", "hgks_set_grid_cap",
+    "hgks_launch_count", "hgks_set_kernel_timing", "hgks_kernel_times", "hgks_set_graphs", "hgks_set_grid_cap", "hgks_set_race_shake",
     "hgks_measure_fp64_peak",
 ]
 
@@ -84,6 +84,7 @@ def load():
     L.hgks_residual.argtypes = [sp, _dp, ctypes.c_double, _dp, _dp, _dp, _dp, _dp]
     L.hgks_apply_inverse_mass.argtypes = [sp, _dp, _dp]
     L.hgks_compute_dt.argtypes = [sp, ctypes.c_double, _dp]
+    L.hgks_compute_dt_k.argtypes = [sp, ctypes.c_double, ctypes.c_int, _dp]
     L.hgks_step.argtypes = [sp, ctypes.c_double]
     L.hgks_two_stage_step_host.argtypes = [sp, _dp, ctypes.c_double]
     L.hgks_two_stage_step_host_streamed.argtypes = [sp, _dp, ctypes.c_double, ctypes.c_int]
@@ -121,6 +122,8 @@ def load():
     L.hgks_set_graphs.restype = None
     L.hgks_set_grid_cap.argtypes = [sp, ctypes.c_int]
     L.hgks_set_grid_cap.restype = None
+    L.hgks_set_race_shake.argtypes = [sp, ctypes.c_uint]
+    L.hgks_set_race_shake.restype = None
     L.hgks_set_stream.argtypes = [sp, sp]
     L.hgks_get_stream.argtypes = [sp]
     L.hgks_get_stream.restype = sp

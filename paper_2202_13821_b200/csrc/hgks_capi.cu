@@ -91,6 +91,7 @@ struct hgks_solver {
     double g_cfl = -1.0;
     int g_fixed = -1;
     int grid_cap = 0;
+    unsigned shake = 0;
     bool count_fluxes = false;
     long flux_evals = 0;
     long launches = 0;
@@ -172,6 +173,7 @@ KParams make_params(hgks_solver* s, int stage, int slot) {
     kp.scal = scal_slot(s, slot);
     kp.two_mu = 2.0 * s->cfg.mu;
     kp.grid_cap = s->grid_cap;
+    kp.shake = s->shake;
     kp.gas.gamma = s->cfg.gamma;
     kp.gas.gm1 = s->cfg.gamma - 1.0;
     kp.gas.K = (5.0 - 3.0 * s->cfg.gamma) / (s->cfg.gamma - 1.0);
@@ -440,7 +442,7 @@ int finish_error(hgks_solver* s, unsigned long long key, double* const stage_inp
 }
 
 // compute_dt's state failure: the bare state error (not wrapped in worker_error)
-int finish_dt_error(hgks_solver* s, unsigned long long key, const double* q, double cfl) {
+int finish_dt_error(hgks_solver* s, unsigned long long key, const double* q, double cfl, int degree) {
     const long item = (long)((key >> 22) & ((1ull << 39) - 1));
     const int code = (int)(key & 0xff);
     KParams kp = make_params(s, 0, 0);
@@ -448,7 +450,7 @@ int finish_dt_error(hgks_solver* s, unsigned long long key, const double* q, dou
     kp.err_key = s->d_key + K_DTERR;
     double val = 0.0;
     const int rc = report_value(s, owns_item(s, 1, item), [&] {
-        dt_kernel<<<148 * 4, 256, 0, s->stream>>>(kp, q, cfl, s->cfg.degree, s->d_key + K_SCRATCH);
+        dt_kernel<<<148 * 4, 256, 0, s->stream>>>(kp, q, cfl, degree, s->d_key + K_SCRATCH);
     }, &val);
     if (rc) return rc;
     s->e_code = HGKS_ERR_STATE;
@@ -718,12 +720,16 @@ int do_step(hgks_solver* s, double dt) {
     return HGKS_OK;
 }
 
-int compute_dt_host(hgks_solver* s, double cfl, double* dt) {
+// degree: the k of the viscous bound cfl h^2 rho / (2 mu (2k+1)) — an
+// argument of the reference's compute_dt (integrator.hpp:27, :40), by
+// default the solver's own degree
+int compute_dt_host(hgks_solver* s, double cfl, double* dt, int degree = -1) {
+    if (degree < 0) degree = s->cfg.degree;
     int rc = reset_keys(s);
     if (rc) return rc;
     KParams kp = make_params(s, 0, 0);
     kp.err_key = s->d_key + K_DTERR;
-    dt_kernel<<<148 * 4, 256, 0, s->stream>>>(kp, s->qa(), cfl, s->cfg.degree, s->d_key + K_DT);
+    dt_kernel<<<148 * 4, 256, 0, s->stream>>>(kp, s->qa(), cfl, degree, s->d_key + K_DT);
     ++s->launches;
     CK(cudaGetLastError());
     if (s->nccl_on()) {  // (dt error key, dt bits) min over slabs in one call
@@ -737,7 +743,7 @@ int compute_dt_host(hgks_solver* s, double cfl, double* dt) {
     // is left waiting in the next collective)
     if (s->host_hooks() && s->hreduce && s->hreduce(s->hreduce_user, HGKS_REDUCE_MIN_U64, h, 2) != 0)
         return fail(s, HGKS_ERR_CUDA, "host reduce callback failed");
-    if (h[0] != kNoKey) return finish_dt_error(s, h[0], s->qa(), cfl);
+    if (h[0] != kNoKey) return finish_dt_error(s, h[0], s->qa(), cfl, degree);
     double v;
     std::memcpy(&v, &h[1], sizeof v);
     if (!(v > 0.0) || !std::isfinite(v)) return fail(s, HGKS_ERR_DT, "compute_dt: nonpositive dt");
@@ -893,7 +899,7 @@ int advance_device(hgks_solver* s, double t_end, double cfl, double dt_fixed, do
     if (steps) *steps = last.steps;
     if (halted == HALT_DONE) return HGKS_OK;
     if (halted == HALT_DT) return fail(s, HGKS_ERR_DT, "compute_dt: nonpositive dt");
-    if (halted == HALT_DT_STATE) return finish_dt_error(s, last.fail_key, s->buf[ph], cfl);
+    if (halted == HALT_DT_STATE) return finish_dt_error(s, last.fail_key, s->buf[ph], cfl, s->cfg.degree);
     double* const inputs[2] = {s->buf[ph], s->qs};
     rc = finish_error(s, last.fail_key, inputs, ph);
     if (rc == HGKS_ERR_STATE) s->msg += " at t=" + std::to_string(last.t);
@@ -1006,6 +1012,12 @@ int hgks_apply_inverse_mass(hgks_solver* s, const double* R, double* L) {
 int hgks_compute_dt(hgks_solver* s, double cfl, double* dt) {
     GUARD(s);
     return compute_dt_host(s, cfl, dt);
+}
+
+int hgks_compute_dt_k(hgks_solver* s, double cfl, int degree, double* dt) {
+    GUARD(s);
+    if (degree < 1) return fail(s, HGKS_ERR_CONFIG, "compute_dt: degree must be >= 1");
+    return compute_dt_host(s, cfl, dt, degree);
 }
 
 int hgks_step(hgks_solver* s, double dt) {
@@ -1508,6 +1520,11 @@ void hgks_set_graphs(hgks_solver* s, int on) {
 void hgks_set_grid_cap(hgks_solver* s, int ctas) {
     drop_graphs(s);
     s->grid_cap = ctas > 0 ? ctas : 0;
+}
+
+void hgks_set_race_shake(hgks_solver* s, unsigned seed) {
+    drop_graphs(s);
+    s->shake = seed;
 }
 
 int hgks_measure_fp64_peak(int device, double ms, double* tflops) {

@@ -103,6 +103,7 @@ struct KParams {
     const double* scal;
     double two_mu;         // 2 mu: face tau = 2 mu / (p_l + p_r)
     int grid_cap;          // > 0: cap on the persistent grids (tests: many tiles per CTA)
+    unsigned shake;        // != 0: race shaker seed (tests; see race_shake)
     GasC gas;
     const double* dx;      // [nx] widths
     const double* dy;      // [ny]
@@ -126,6 +127,22 @@ __device__ __forceinline__ unsigned long long err_key(int stage, int phase, long
     return ((unsigned long long)stage << 62) | ((unsigned long long)phase << 61) |
            ((unsigned long long)item << 22) | ((unsigned long long)point << 12) |
            ((unsigned long long)sub << 8) | (unsigned long long)code;
+}
+
+// Race shaker (test hook, KParams::shake != 0): before every cp.async wait
+// and barrier, each warp sleeps a pseudo-random 0..4 us keyed by (seed, CTA,
+// warp, site, tile), so a missing barrier or a wrong cp.async group count
+// shows up as a changed result against the unperturbed run (bitwise). It
+// stands in for compute-sanitizer racecheck, which this GPU pool does not run.
+__device__ __forceinline__ void race_shake(const KParams& kp, int site, int n) {
+    if (kp.shake) {
+        unsigned h = kp.shake * 2654435761u ^ (blockIdx.x * 40503u) ^ ((threadIdx.x >> 5) * 9973u) ^
+                     ((unsigned)site * 7919u) ^ ((unsigned)n * 104729u);
+        h ^= h >> 13;
+        h *= 0x5bd1e995u;
+        h ^= h >> 15;
+        __nanosleep(h & 4095u);
+    }
 }
 
 __device__ __forceinline__ void report_error(const KParams& kp, unsigned long long key,
@@ -408,6 +425,7 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
         }
         const int i0 = cur.i0, j = cur.j, k = cur.k;
         const int i = i0 + lane;
+        race_shake(kp, 0, n);
         if (HGKS_FACE_STAGES == 2) cp_async_wait<1>();  // this tile's stage
         else cp_async_wait<0>();
         __syncthreads();
@@ -516,6 +534,7 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
             }
         }
         }  // points of this warp
+        race_shake(kp, 1, n);
         __syncthreads();  // this stage is free for the prefetch two tiles ahead
         if (HGKS_FACE_STAGES == 1) {
             if (has_next) prefetch(nxt, smem);
@@ -622,7 +641,7 @@ enum : int { MODE_RESIDUAL = 0, MODE_STAGE1 = 1, MODE_STAGE2 = 2 };
 template <int P, int DIM, int MODE>
 struct CellTile {
     using SH = Shape<P, DIM>;
-    static constexpr int TC = SH::TC, NC = SH::NC, NVP = SH::NVP;
+    static constexpr int TC = SH::TC, NC = SH::NC, NVP = SH::NVP, N = SH::N;
     static constexpr int NFX = SH::template nfp<0>(), NFY = SH::template nfp<1>(),
                          NFZ = SH::template nfp<2>();
     static constexpr int RW = MODE == MODE_STAGE2 ? 5 : 10, RO = 10 - RW;
@@ -632,25 +651,43 @@ struct CellTile {
     static constexpr int FZ = NFZ * RW * 2 * TC;   // z faces layers k, k+1
     static constexpr int VFW = 3 * RW;             // flux rows per volume point
     static constexpr int VF = NVP * VFW * TC;      // volume-point fluxes [p][VFW][TC]
-    static constexpr int LB = MODE == MODE_STAGE1 ? 2 * NC * TC : 0;  // L, Lt of the tile (stage-1 q*)
     static constexpr int GEO = 2 * TC + 4;          // widths of a tile: dx, 2/dx [TC]; dy, dz, 2/dy, 2/dz
     // stage 2: the tile's A = q + dt L1 + dt^2/6 Lt1 [NC][TC], prefetched with the faces
     static constexpr int AB = MODE == MODE_STAGE2 ? COEF : 0;
-    static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + LB + 2 * GEO + AB;
     // threads / resident CTAs: stage 2 (half the tile, ~150 registers) runs
     // one thread per (cell, volume point) at 3 CTAs per SM for 3-D P1/P2
     static constexpr bool S2X = MODE == MODE_STAGE2 && P < 3 && DIM == 3;
     static constexpr int NT = S2X ? TC * NVP : SH::NT_CELL;
     static constexpr int MINB = S2X ? 3 : SH::MINB_CELL;
+    // projection items (cell, var, F|Ft); stage 2 projects only Ft
+    static constexpr int NITEMS = TC * 5 * (MODE == MODE_STAGE2 ? 1 : 2);
+    // phase B occupies the first NBT threads; when whole warps are left over
+    // (3-D P1/P2, 160 threads: warp 4) they are the FACE warps: they fetch the
+    // tile's face fluxes themselves and reduce the face part of every
+    // projection item while phase B runs (the cell kernel's idle warp of
+    // phase B in the one-phase-at-a-time design)
+    static constexpr int NBT = ((TC * NVP + 31) / 32) * 32;
+    static constexpr bool FCW = NT - NBT >= 32;
+    static constexpr int RF = FCW ? N * NITEMS : 0;  // face parts of the items [m][item]
+    static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + RF + 2 * GEO + AB;
 };
 
 // Persistent CTA over tiles of TC consecutive cells along x, software
-// pipelined: while tile t is computed, the coefficients of tile t+grid and
-// the face fluxes of tile t stream into shared memory (cp.async).
-// Phase B: one (cell, volume point) item per thread -> smooth fluxes.
-// Phase C: one (cell, var, F|Ft) item per thread -> face gather + volume
-// projection + M^-1 (+ S2O4 combine); stage 1 then forms q* per coefficient
-// from shared memory, stage 2 needs only Lt2.
+// pipelined with TWO CTA barriers per tile:
+//   top:  the tile's coefficients / widths (prefetched a tile ahead) landed
+//         -> barrier -> issue this tile's face fluxes (+ stage 2's A tile)
+//         and the next tile's coefficients
+//   phase B (threads < NBT): one (cell, volume point) item per thread ->
+//         smooth fluxes at the volume points (vf)
+//   face warps (FCW): meanwhile the face part of every projection item
+//         (+ w jac B- F(minus) - w jac B+ F(plus)) into rf
+//   barrier (vf, rf / the faces complete)
+//   phase C: one (cell, var, F|Ft) item per thread -> volume projection,
+//         M^-1 and the fused S2O4 combine; the F and Ft items of a (cell,
+//         var) sit in adjacent lanes and swap L / Lt with one shuffle, so
+//         stage 1 writes q* (F lane) and A (Ft lane) with no barrier.
+// Nothing a tile writes in shared memory is read after the next top barrier,
+// so no end-of-tile barrier is needed.
 template <int P, int DIM, bool VISC, int MODE>
 __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, MODE>::MINB)
     cell_kernel(KParams kp, const double* __restrict__ qin, const double* __restrict__ f0,
@@ -662,15 +699,16 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
     using SH = Shape<P, DIM>;
     using CT = CellTile<P, DIM, MODE>;
     constexpr int N = SH::N, NC = SH::NC, NVP = SH::NVP, TC = SH::TC;
-    constexpr int NT = CT::NT, NAX = SH::NAX;
+    constexpr int NT = CT::NT, NAX = SH::NAX, NITEMS = CT::NITEMS, NBT = CT::NBT;
+    constexpr bool FCW = CT::FCW;
     extern __shared__ double smem[];
     double* coefb = smem;                 // [2][NC][TC]
     double* fx = coefb + 2 * CT::COEF;
     double* fy = fx + CT::FX;
     double* fz = fy + CT::FY;
     double* vf = fz + CT::FZ;             // [NVP][VFW][TC]
-    double* lb = vf + CT::VF;             // [2][NC][TC]
-    double* geob = lb + CT::LB;           // [2][GEO], staged with the coefficients
+    double* rf = vf + CT::VF;             // [N][NITEMS] face parts (FCW)
+    double* geob = rf + CT::RF;           // [2][GEO], staged with the coefficients
     double* ab = geob + 2 * CT::GEO;      // [NC][TC] stage 2: A of the tile
 
     const int tid = threadIdx.x;
@@ -720,8 +758,10 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
     // stage 2 consumes only the Ft rows (the face pass stores only those)
     constexpr int RW = CT::RW, RO = CT::RO;
     auto face_row = [](int rr) { return (rr / RW) * 10 + RO + rr % RW; };
-    auto prefetch_faces = [&](const TI& ti) {
-        if (MODE == MODE_STAGE2) prefetch_state(L1, ti, ab);
+    // the tile's face fluxes, issued by threads [t0, t0 + nthr) (the face
+    // warps on the FCW path, else every thread)
+    auto prefetch_faces = [&](const TI& ti, int t0, int nthr) {
+        const int ltid = tid - t0;
         const int i0 = ti.i0, j = ti.j, k = ti.k;
         const long rowk = (long)nx * (j + (long)ny * k);
         const int jp = j + 1 == ny ? 0 : j + 1;
@@ -731,8 +771,8 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
         if constexpr (2 * TC == 32) {
             // one face row per warp instruction: x rows hold TC+1 faces
             // (lanes 0..TC), y/z rows the TC faces of both neighbour rows
-            constexpr int NW = NT / 32;
-            const int lane = tid & 31, warp = tid >> 5;
+            const int NW = nthr / 32;
+            const int lane = ltid & 31, warp = ltid >> 5;
             const int igx = i0 + lane;
             const bool okx = lane <= TC && igx <= nx;  // x is periodic: face nx is face 0
             const long ox = rowk + (okx ? (igx == nx ? 0 : igx) : 0);
@@ -759,20 +799,20 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
                     cp_async8(fz + (pf * RW + c) * 2 * TC + lane, sz + pf * pst, ok);
             }
         } else {
-            for (int e = tid; e < CT::NFX * RW * (TC + 1); e += NT) {  // x faces i0 .. i0+TC (periodic wrap at nx)
+            for (int e = ltid; e < CT::NFX * RW * (TC + 1); e += nthr) {  // x faces i0 .. i0+TC (periodic wrap at nx)
                 const int l = e % (TC + 1), r = face_row(e / (TC + 1));
                 const int ig = i0 + l;
                 const bool ok = ig <= nx;  // x is always periodic: face nx is face 0
                 const int iw = ig == nx ? 0 : ig;
                 cp_async8(fx + e, f0 + (long)r * kp.fs + rowk + (ok ? iw : 0), ok);
             }
-            for (int e = tid; e < CT::NFY * RW * 2 * TC; e += NT) {  // y faces of rows j, j+1
+            for (int e = ltid; e < CT::NFY * RW * 2 * TC; e += nthr) {  // y faces of rows j, j+1
                 const int l = e % (2 * TC), r = face_row(e / (2 * TC));
                 const int ig = i0 + (l % TC);
                 const bool ok = ig < nx;
                 cp_async8(fy + e, f1 + (long)r * kp.fs + (l < TC ? rowk : rowp) + (ok ? ig : 0), ok);
             }
-            for (int e = tid; e < CT::NFZ * RW * 2 * TC; e += NT) {  // z faces of layers k, k+1
+            for (int e = ltid; e < CT::NFZ * RW * 2 * TC; e += nthr) {  // z faces of layers k, k+1
                 const int l = e % (2 * TC), r = face_row(e / (2 * TC));
                 const int ig = i0 + (l % TC);
                 const bool ok = ig < nx;
@@ -780,6 +820,60 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
             }
         }
     };
+    // projection item -> (cell column l, variable v, F (0) | Ft (1)); the F
+    // and Ft items of a (cell, var) are adjacent lanes (stage 1 / residual)
+    auto item_of = [](int it, int& l, int& v, int& ft) {
+        if (MODE == MODE_STAGE2) {
+            ft = 1;
+            l = it % TC;
+            v = it / TC;
+        } else {
+            ft = it & 1;
+            l = (it >> 1) % TC;
+            v = (it >> 1) / TC;
+        }
+    };
+    // face part of item it (dg.hpp:404-425): + w jac B- F(minus face) - w jac
+    // B+ F(plus face), with the Legendre parity B+(p,n) = (-1)^{n_a} B-(p,n)
+    auto face_part = [&](int it, const double* gg, double hy, double hz, double* R) {
+        int l, v, ft;
+        item_of(it, l, v, ft);
+        const int row = 5 * ft + v;
+        const double hx = gg[l];
+        const double jac[3] = {hy * hz * 0.25, hz * hx * 0.25, hx * hy * 0.25};
+#pragma unroll
+        for (int m = 0; m < N; ++m) R[m] = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int nfp = a == 0 ? CT::NFX : a == 1 ? CT::NFY : CT::NFZ;
+            double acc[N];
+#pragma unroll
+            for (int m = 0; m < N; ++m) acc[m] = 0.0;
+#pragma unroll
+            for (int pf = 0; pf < nfp; ++pf) {
+                const int r = pf * RW + row - RO;
+                double Fm, Fp;
+                if (a == 0) {
+                    Fm = fx[r * (TC + 1) + l];
+                    Fp = fx[r * (TC + 1) + l + 1];
+                } else {
+                    const double* fa = a == 1 ? fy : fz;
+                    Fm = fa[r * 2 * TC + l];
+                    Fp = fa[r * 2 * TC + TC + l];
+                }
+                const double Dm = Fm - Fp, Sm = Fm + Fp;
+#pragma unroll
+                for (int m = 0; m < N; ++m) {
+                    const double c = ctab<P, DIM>.fw[a][pf] * ctab<P, DIM>.fB[a][0][pf][m];
+                    const bool odd = ctab<P, DIM>.par[a][m] != 0;
+                    if (c != 0.0) acc[m] += c * (odd ? Sm : Dm);
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < N; ++m) R[m] += jac[a] * acc[m];
+        }
+    };
+
     if (kp.scal[SC_ACTIVE] == 0.0) return;  // halted device loop: no-op step
     const double dt = kp.scal[SC_DT];
     const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
@@ -789,91 +883,83 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
     int n = 0;
     for (int t = t0; t < tile_end; t += step, ++n) {
         double* sc = coefb + (n & 1) * CT::COEF;
-        prefetch_faces(cur);
-        cp_async_commit();
         const bool has_next = t + step < tile_end;
         const TI nxt = walk.next(cur);
-        if (has_next) prefetch_coef(nxt, coefb + ((n + 1) & 1) * CT::COEF, geob + ((n + 1) & 1) * CT::GEO);
-        cp_async_commit();
         const int i0 = cur.i0, j = cur.j, k = cur.k;
         const long cbase = (long)(k + 1) * kp.S + (long)j * nx;
         const double* gg = geob + (n & 1) * CT::GEO;
         const long cglob_row = (long)nx * (j + (long)ny * (k + kp.kglob0));
-        cp_async_wait<2>();  // this tile's coefficients and widths
-        __syncthreads();
+        race_shake(kp, 2, n);
+        cp_async_wait<0>();  // this tile's coefficients and widths (issued a tile ahead)
+        __syncthreads();     // ... visible to all; the previous tile's buffers are free
+        // face fluxes of this tile (+ stage 2's A tile), then the next tile's
+        // coefficients; the face warps fetch their own faces
+        if (MODE == MODE_STAGE2) prefetch_state(L1, cur, ab);
+        if (!FCW) prefetch_faces(cur, 0, NT);
+        else if (tid >= NBT) prefetch_faces(cur, NBT, NT - NBT);
+        cp_async_commit();
+        if (has_next) prefetch_coef(nxt, coefb + ((n + 1) & 1) * CT::COEF, geob + ((n + 1) & 1) * CT::GEO);
+        cp_async_commit();
         const double hy = gg[2 * TC], hz = gg[2 * TC + 1];
         const double i2hy = gg[2 * TC + 2], i2hz = gg[2 * TC + 3];
 
-        // ---- phase B: smooth fluxes at volume points
-        for (int it = tid; it < TC * NVP; it += NT) {
-            const int l = it % TC;
-            const int p = SH::NQ == 2 ? it / TC : kVolOrder<P, DIM>.p[it / TC];
-            const int i = i0 + l;
-            if (i >= nx) continue;
-            const double i2h[3] = {gg[TC + l], i2hy, i2hz};
-            double e[20];
-            vol_eval_sym<P, DIM, TC>(p, sc + l, i2h, e);
-            double o[30];
-            double bad = 0.0;
-            const int rc = smooth_flux<VISC, NAX, MODE == MODE_STAGE2>(e, kp.gas, o, bad);
-            if (rc) {
-                report_error(kp, err_key(kp.stage, 1, cglob_row + i, p, 0, rc), bad);
+        if (!FCW || tid < NBT) {
+            // ---- phase B: smooth fluxes at volume points
+            for (int it = tid; it < TC * NVP; it += (FCW ? NBT : NT)) {
+                const int l = it % TC;
+                const int p = SH::NQ == 2 ? it / TC : kVolOrder<P, DIM>.p[it / TC];
+                const int i = i0 + l;
+                if (i >= nx) continue;
+                const double i2h[3] = {gg[TC + l], i2hy, i2hz};
+                double e[20];
+                vol_eval_sym<P, DIM, TC>(p, sc + l, i2h, e);
+                double o[30];
+                double bad = 0.0;
+                const int rc = smooth_flux<VISC, NAX, MODE == MODE_STAGE2>(e, kp.gas, o, bad);
+                if (rc) {
+                    report_error(kp, err_key(kp.stage, 1, cglob_row + i, p, 0, rc), bad);
 #pragma unroll
-                for (int m = 0; m < 30; ++m) o[m] = 0.0;
+                    for (int m = 0; m < 30; ++m) o[m] = 0.0;
+                }
+#pragma unroll
+                for (int m = 0; m < 10 * NAX; ++m)
+                    if (m % 10 >= RO) vf[(p * CT::VFW + (m / 10) * RW + m % 10 - RO) * TC + l] = o[m];
             }
+        } else if constexpr (FCW) {
+            // ---- face warps: the face part of every projection item
+            if (!kp.report) {
+                cp_async_wait<1>();  // their own face copies (the coefficient group may still fly)
+                __syncwarp();
+                for (int it = tid - NBT; it < NITEMS; it += NT - NBT) {
+                    double R[N];
+                    face_part(it, gg, hy, hz, R);
 #pragma unroll
-            for (int m = 0; m < 10 * NAX; ++m)
-                if (m % 10 >= RO) vf[(p * CT::VFW + (m / 10) * RW + m % 10 - RO) * TC + l] = o[m];
+                    for (int m = 0; m < N; ++m) rf[m * NITEMS + it] = R[m];
+                }
+            }
         }
         if (kp.report) return;
-        cp_async_wait<1>();  // this tile's face fluxes
+        race_shake(kp, 3, n);
+        if (!FCW) cp_async_wait<1>();  // this tile's face fluxes
         __syncthreads();
 
-        // ---- phase C: gather + projection + inverse mass (+ stage-2 combine)
-        constexpr int FT0 = MODE == MODE_STAGE2 ? 1 : 0;
-        constexpr int NITEMS = TC * 5 * (2 - FT0);
-        for (int it = tid; it < NITEMS; it += NT) {
-            const int l = it % TC, vv = it / TC;
-            const int v = vv % 5, ft = FT0 + vv / 5;  // ft: 0 -> F (R), 1 -> Ft (Rt)
+        // ---- phase C: volume projection + face part + inverse mass (+ combine)
+        for (int it0 = 0; it0 < NITEMS; it0 += NT) {
+            const int it = it0 + tid;
+            if (it >= NITEMS) break;
+            int l, v, ft;
+            item_of(it, l, v, ft);
             const int i = i0 + l;
-            if (i >= nx) continue;
+            const bool valid = i < nx;
             const double hx = gg[l];
             const double i2h[3] = {gg[TC + l], i2hy, i2hz};
             const int row = 5 * ft + v;
             double R[N];
+            if constexpr (FCW) {
 #pragma unroll
-            for (int m = 0; m < N; ++m) R[m] = 0.0;
-            // faces (dg.hpp:404-425): + w jac B- F(minus face) - w jac B+ F(plus face),
-            // with the Legendre parity B+(p,n) = (-1)^{n_a} B-(p,n)
-            const double jac[3] = {hy * hz * 0.25, hz * hx * 0.25, hx * hy * 0.25};
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                const int nfp = a == 0 ? CT::NFX : a == 1 ? CT::NFY : CT::NFZ;
-                double acc[N];
-#pragma unroll
-                for (int m = 0; m < N; ++m) acc[m] = 0.0;
-#pragma unroll
-                for (int pf = 0; pf < nfp; ++pf) {
-                    const int r = pf * RW + row - RO;
-                    double Fm, Fp;
-                    if (a == 0) {
-                        Fm = fx[r * (TC + 1) + l];
-                        Fp = fx[r * (TC + 1) + l + 1];
-                    } else {
-                        const double* fa = a == 1 ? fy : fz;
-                        Fm = fa[r * 2 * TC + l];
-                        Fp = fa[r * 2 * TC + TC + l];
-                    }
-                    const double Dm = Fm - Fp, Sm = Fm + Fp;
-#pragma unroll
-                    for (int m = 0; m < N; ++m) {
-                        const double c = ctab<P, DIM>.fw[a][pf] * ctab<P, DIM>.fB[a][0][pf][m];
-                        const bool odd = ctab<P, DIM>.par[a][m] != 0;
-                        if (c != 0.0) acc[m] += c * (odd ? Sm : Dm);
-                    }
-                }
-#pragma unroll
-                for (int m = 0; m < N; ++m) R[m] += jac[a] * acc[m];
+                for (int m = 0; m < N; ++m) R[m] = rf[m * NITEMS + it];
+            } else {
+                face_part(it, gg, hy, hz, R);
             }
             // volume (dg.hpp:427-448): + w (h0 h1 h2 / 8) (2/h_a) dB_a F_a
             const double vol = hx * hy * hz;
@@ -899,46 +985,42 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
             const long g0 = (long)v * kp.cs + cbase + i;
             if (MODE == MODE_RESIDUAL) {
                 double* o = ft ? out1 : out0;
+                if (valid) {
 #pragma unroll
-                for (int m = 0; m < N; ++m) o[g0 + (long)(m * 5) * kp.cs] = R[m];
+                    for (int m = 0; m < N; ++m) o[g0 + (long)(m * 5) * kp.cs] = R[m];
+                }
             } else {
                 // mass_diag (dg.hpp:42-50): 1/M_n = (2nx+1)(2ny+1)(2nz+1)/vol (solver.hpp:49-51)
                 const double ivol = 1.0 / vol;
                 const double c6 = dt * dt / 6.0;
+                if (MODE == MODE_STAGE1) {
+                    // the partner lane holds the other of (L1, Lt1) of this (cell, var):
+                    //   q* = q + dt/2 L1 + dt^2/8 Lt1   (F lane -> out0)
+                    //   A  = q + (dt L1 + dt^2/6 Lt1)   (Ft lane -> out1; stage 2 adds dt^2/6 * 2 Lt2)
+                    // lanes of this warp holding an item (pairs never straddle it)
+                    const int wl = it0 + (tid & ~31);
+                    const unsigned mask = wl + 32 <= NITEMS ? 0xffffffffu : (1u << (NITEMS - wl)) - 1u;
 #pragma unroll
-                for (int m = 0; m < N; ++m) {
-                    const double L = R[m] * (ctab<P, DIM>.massf[m] * ivol);
-                    const long gi = g0 + (long)(m * 5) * kp.cs;
-                    if (MODE == MODE_STAGE1) {
-                        lb[(ft * NC + m * 5 + v) * TC + l] = L;
-                    } else {
-                        // q^{n+1} = q + dt L1 + dt^2/6 (Lt1 + 2 Lt2) (integrator.hpp:72-74)
-                        // = A + dt^2/6 * 2 Lt2, A formed by stage 1
-                        out0[gi] = ab[(m * 5 + v) * TC + l] + c6 * (2.0 * L);
+                    for (int m = 0; m < N; ++m) {
+                        const double L = R[m] * (ctab<P, DIM>.massf[m] * ivol);
+                        const double Lo = __shfl_xor_sync(mask, L, 1);
+                        const double q = sc[(m * 5 + v) * TC + l];
+                        const double Lf = ft ? Lo : L, Lt = ft ? L : Lo;
+                        const double val = ft ? q + (dt * Lf + c6 * Lt) : q + 0.5 * dt * Lf + 0.125 * dt * dt * Lt;
+                        double* o = ft ? out1 : out0;
+                        if (valid) o[g0 + (long)(m * 5) * kp.cs] = val;
+                    }
+                } else {
+                    // q^{n+1} = q + dt L1 + dt^2/6 (Lt1 + 2 Lt2) (integrator.hpp:72-74)
+                    //         = A + dt^2/6 * 2 Lt2, A formed by stage 1
+#pragma unroll
+                    for (int m = 0; m < N; ++m) {
+                        const double L = R[m] * (ctab<P, DIM>.massf[m] * ivol);
+                        if (valid) out0[g0 + (long)(m * 5) * kp.cs] = ab[(m * 5 + v) * TC + l] + c6 * (2.0 * L);
                     }
                 }
             }
         }
-        if (MODE == MODE_STAGE1) {
-            // from shared memory, per coefficient (integrator.hpp:69-74):
-            //   q* = q + dt/2 L1 + dt^2/8 Lt1           -> out0
-            //   A  = q + (dt L1 + dt^2/6 Lt1)           -> out1 (stage 2 adds dt^2/6 * 2 Lt2)
-            __syncthreads();
-            const double c6 = dt * dt / 6.0;
-            // unrolled with predicated stores: all shared-memory loads of the
-            // thread's elements issue before the first use
-#pragma unroll
-            for (int e = tid; e < NC * TC; e += NT) {
-                const int l = e % TC, comp = e / TC;
-                const double q = sc[comp * TC + l], L = lb[comp * TC + l], Lt = lb[(NC + comp) * TC + l];
-                const long gi = comp * kp.cs + cbase + i0 + l;
-                if (i0 + l < nx) {
-                    out0[gi] = q + 0.5 * dt * L + 0.125 * dt * dt * Lt;
-                    out1[gi] = q + (dt * L + c6 * Lt);
-                }
-            }
-        }
-        __syncthreads();  // buffers of this tile are free for the next prefetch
         cur = nxt;
     }
     cp_async_wait<0>();

@@ -462,6 +462,11 @@ class Solver:
         """Test hook: cap the persistent grids (every CTA walks many tiles)."""
         self.L.hgks_set_grid_cap(self.h, int(ctas))
 
+    def set_race_shake(self, seed: int):
+        """Test hook: randomized per-warp delays before every cp.async wait and
+        barrier of the persistent kernels (0 = off)."""
+        self.L.hgks_set_race_shake(self.h, int(seed))
+
 
 def measure_fp64_peak(device: int = 0, ms: float = 50.0) -> float:
     """Sustained DFMA throughput (TFLOP/s) of the device: the FP64 roofline

@@ -268,3 +268,28 @@ def test_nccl_self_ring_bitwise(hgks):
     b.solver.advance_records(1e9, 0.15, max_steps=4)
     assert np.array_equal(a.solver.get_state()[0], b.solver.get_state()[0])
     assert np.allclose(b.solver.slab_reduce_sum([1.5, -2.0]), [1.5, -2.0])
+
+
+# ------------------------------------------------ race shaker (no racecheck here)
+@pytest.mark.parametrize("case,n,degree,cap", [("tgv", 8, 2, 2), ("tgv", 8, 3, 2), ("adv3d", 12, 1, 3),
+                                               ("vortex2d", 12, 2, 2), ("tgv", 16, 2, 0)])
+def test_race_shaker_bitwise(hgks, case, n, degree, cap):
+    """compute-sanitizer is closed on this GPU pool, so races are hunted by
+    perturbation: pseudo-random per-warp sleeps before every cp.async wait and
+    barrier (hgks_set_race_shake) must not change a single bit of the
+    residual, the faces, the host-dt steps or the device loop."""
+    P = hgks
+    cfl = P.default_cfl(degree)
+    outs = []
+    for seed in (0, 1, 7, 12345):
+        r = P.setup_run(P.CaseConfig.named(case, n), P.RunOptions(degree=degree))
+        s = r.solver
+        s.set_grid_cap(cap)
+        s.set_race_shake(seed)
+        res = s.residual(s.compute_dt(cfl), faces=True)
+        s.step(s.compute_dt(cfl))
+        s.advance_records(1e9, cfl, max_steps=2)
+        outs.append([res["R"], res["Rt"], *res["faces"], s.get_state()[0]])
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
