@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=32, help="z-chunks of the streamed host-vector step")
     ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of CPU reference work")
+    ap.add_argument("--face-staging", default="tma", choices=["tma", "cpasync"],
+                    help="face-kernel staging: TMA boxes (default) or per-lane cp.async (A/B)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo = host-staged halo exchange (multi-rank test mode on one GPU)")
     return ap.parse_args()
@@ -231,6 +233,7 @@ def main():
     stream = torch.cuda.Stream(local)
     torch.cuda.set_stream(stream)
     s.set_stream(stream.cuda_stream)
+    s.set_face_tma(a.face_staging == "tma")
     if world > 1:
         # nccl: the library's own data plane (halo send/recv, dt and error-key
         # reductions inside the per-step graph); gloo: the host-staged test mode
@@ -272,13 +275,16 @@ def main():
     # ---- per-kernel split (outside the timed region): CUDA events around the
     # face pass and the cell kernel of each stage, host-dt steps
     s.set_kernel_timing(True)
-    face_ms, cell_ms = [], []
+    face_ms, cell_ms, stage_ms = [], [], []
     for _ in range(max(3, min(a.steps, 8))):
         s.step(s.compute_dt(cfl))
         f, c = s.kernel_times()
         face_ms.append(f)
         cell_ms.append(c)
+        stage_ms.append([s.kernel_times_stage(0), s.kernel_times_stage(1)])
     s.set_kernel_timing(False)
+    per_stage = {f"stage{st + 1}": {"face_ms": statistics.median(x[st][0] for x in stage_ms),
+                                    "cell_ms": statistics.median(x[st][1] for x in stage_ms)} for st in range(2)}
 
     # ---- e2e through the C ABI with host buffers (rank-local state)
     e2e = None
@@ -415,6 +421,7 @@ def main():
                           "stage (profiles/kernel_traffic.json)",
         "peak_source": "live DFMA microbenchmark on this GPU (MEASURED_PEAKS.json has no FP64 entry)",
         "hbm": hbm,
+        "per_stage_ms": per_stage,
         "flops_basis": basis,
         "executed": executed,
         "reference_op_basis": ref_basis,
@@ -440,6 +447,7 @@ def main():
         "config": {"workload": workload(a), "case": a.case, "n": a.n, "degree": a.degree,
                    "cells": ncell_glob, "dof": dof_glob, "parallelism": f"z-slab x{world}",
                    "halo_transport": a.dist_backend if world > 1 else None,
+                   "face_staging": a.face_staging,
                    "l2": "inputs larger than L2 (state 839 MB at 128^3 P2); no flush"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -229,6 +229,8 @@ long hgks_launch_count(const hgks_solver* s);
  * the solver stream) when timing is enabled */
 void hgks_set_kernel_timing(hgks_solver* s, int on);
 int hgks_kernel_times(hgks_solver* s, double* face_ms, double* cell_ms, double* other_ms);
+/* the same per S2O4 stage (0 or 1) of the last timed step */
+int hgks_kernel_times_stage(hgks_solver* s, int stage, double* face_ms, double* cell_ms);
 /* CUDA graphs for the device-resident advance loop (default on; kernel
  * timing disables them) */
 void hgks_set_graphs(hgks_solver* s, int on);
@@ -239,6 +241,9 @@ void hgks_set_grid_cap(hgks_solver* s, int ctas);
  * pseudo-random 0..4 us before each cp.async wait and barrier (a race
  * shaker: results must stay bitwise identical); 0 = off */
 void hgks_set_race_shake(hgks_solver* s, unsigned seed);
+/* face-kernel staging: 1 (default) = TMA boxes (cp.async.bulk.tensor +
+ * mbarrier) when nx is even, 0 = per-lane cp.async (A/B and tests) */
+void hgks_set_face_tma(hgks_solver* s, int on);
 
 /* Roofline denominator: sustained FP64 FMA throughput of `device`, measured
  * with a DFMA-chain kernel over ~`ms` milliseconds (CUDA events). Writes

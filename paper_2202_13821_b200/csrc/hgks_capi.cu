@@ -5,6 +5,8 @@
 // no CPU path: every entry point that computes runs the CUDA kernels of
 // hgks_kernels.cuh / hgks_aux_kernels.cuh and reports HGKS_ERR_CUDA if it
 // cannot.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -60,6 +62,11 @@ struct hgks_solver {
     cudaStream_t st_up = nullptr, st_dn = nullptr;
     std::vector<cudaEvent_t> ev_up, ev_c2, ev_dn;
     double* face[3] = {nullptr, nullptr, nullptr};
+    // TMA tensor maps (x, row, comp) of buf[0], buf[1], qs for the TMA-staged
+    // face kernels (KernelSet::face_tma): [array][box 32 | box 34]
+    CUtensorMap qmap[3][2];
+    bool have_qmap = false;  // maps built (even nx)
+    bool face_tma = true;    // use them (hgks_set_face_tma)
     unsigned long long* d_key = nullptr;  // K_* words (hgks_aux_kernels.cuh)
     double* d_val = nullptr;              // report value of a failure
     double* d_red = nullptr;              // reduction scratch
@@ -98,6 +105,7 @@ struct hgks_solver {
     bool timing = false;
     cudaEvent_t ev[6] = {};
     double t_face = 0, t_cell = 0, t_other = 0;
+    double t_stage[2][2] = {{0, 0}, {0, 0}};  // [stage][face, cell] of the last timed step
     // last error
     std::string msg;
     int e_code = 0, e_phase = -1;
@@ -154,6 +162,43 @@ struct DevGuard {
 
 double* scal_slot(hgks_solver* s, int slot) { return s->d_scal + slot * SC_SLOT; }
 
+// tensor map of a state array (null when the face kernels stage by cp.async)
+const CUtensorMap* qmap_of(hgks_solver* s, const double* a) {
+    if (!s->have_qmap || !s->face_tma) return nullptr;
+    if (a == s->buf[0]) return s->qmap[0];
+    if (a == s->buf[1]) return s->qmap[1];
+    if (a == s->qs) return s->qmap[2];
+    return nullptr;
+}
+
+// 3-D view of a SoA state array for TMA: x (nx, contiguous), row = j + ny *
+// (k + 1) over the owned layers and both ghost layers, comp (NC, stride cs);
+// box = one x tile of 32 cells x all components (the face kernel's stage)
+int make_qmaps(hgks_solver* s) {
+    if (!s->ks.face_tma) return HGKS_OK;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(s, HGKS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    if ((s->nx * 8) % 16 != 0) return HGKS_OK;  // TMA global strides are 16-byte multiples: cp.async path
+    auto encode = (PFN_cuTensorMapEncodeTiled)fn;
+    double* arrs[3] = {s->buf[0], s->buf[1], s->qs};
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 2; ++b) {
+            const cuuint64_t dims[3] = {(cuuint64_t)s->nx, (cuuint64_t)s->ny * (s->nzl + 2), (cuuint64_t)s->NC};
+            const cuuint64_t strides[2] = {(cuuint64_t)s->nx * 8, (cuuint64_t)s->cs * 8};
+            const cuuint32_t box[3] = {b == 0 ? 32u : 34u, 1, (cuuint32_t)s->NC};
+            const cuuint32_t estr[3] = {1, 1, 1};
+            const CUresult r = encode(&s->qmap[a][b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, arrs[a], dims, strides, box,
+                                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS)
+                return fail(s, HGKS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+        }
+    s->have_qmap = true;
+    return HGKS_OK;
+}
+
 KParams make_params(hgks_solver* s, int stage, int slot) {
     KParams kp{};
     kp.nx = s->nx;
@@ -174,6 +219,7 @@ KParams make_params(hgks_solver* s, int stage, int slot) {
     kp.two_mu = 2.0 * s->cfg.mu;
     kp.grid_cap = s->grid_cap;
     kp.shake = s->shake;
+    kp.face_tma = s->have_qmap && s->face_tma ? 1 : 0;
     kp.gas.gamma = s->cfg.gamma;
     kp.gas.gm1 = s->cfg.gamma - 1.0;
     kp.gas.K = (5.0 - 3.0 * s->cfg.gamma) / (s->cfg.gamma - 1.0);
@@ -333,9 +379,10 @@ int run_residual(hgks_solver* s, double* in, int stage, int slot, int mode, doub
             return fail(s, HGKS_ERR_CUDA, "halo exchange start callback failed");
         }
         ev_record(s, stage * 3 + 0);
-        s->ks.face_axis(kp, 0, in, s->face[0], s->stream, 0, s->nzl);
-        s->ks.face_axis(kp, 1, in, s->face[1], s->stream, 0, s->nzl);
-        s->ks.face_axis(kp, 2, in, s->face[2], s->stream, 1, s->nzl);
+        const CUtensorMap* qm = qmap_of(s, in);
+        s->ks.face_axis(kp, 0, in, qm, s->face[0], s->stream, 0, s->nzl);
+        s->ks.face_axis(kp, 1, in, qm, s->face[1], s->stream, 0, s->nzl);
+        s->ks.face_axis(kp, 2, in, qm, s->face[2], s->stream, 1, s->nzl);
         if (s->nccl_on()) {
             rc = nccl_exchange_finish(s);
             if (rc) return rc;
@@ -344,14 +391,14 @@ int run_residual(hgks_solver* s, double* in, int stage, int slot, int mode, doub
         }
         rc = halo_unpack(s, in);
         if (rc) return rc;
-        s->ks.face_axis(kp, 2, in, s->face[2], s->stream, 0, 1);
-        s->ks.face_axis(kp, 2, in, s->face[2], s->stream, s->nzl, kp.zface_layers);
+        s->ks.face_axis(kp, 2, in, qm, s->face[2], s->stream, 0, 1);
+        s->ks.face_axis(kp, 2, in, qm, s->face[2], s->stream, s->nzl, kp.zface_layers);
         s->launches += 5;
     } else {
         int rc = fill_ghosts(s, in);
         if (rc) return rc;
         ev_record(s, stage * 3 + 0);
-        s->ks.face(kp, in, s->face, s->stream, 0, nullptr);
+        s->ks.face(kp, in, qmap_of(s, in), s->face, s->stream, 0, nullptr);
         s->launches += 3;
     }
     ev_record(s, stage * 3 + 1);
@@ -420,7 +467,7 @@ int finish_error(hgks_solver* s, unsigned long long key, double* const stage_inp
             tile[1] = j;
             tile[2] = k;
             tile[3] = axis;
-            s->ks.face(kp, in, s->face, s->stream, 1, tile);
+            s->ks.face(kp, in, qmap_of(s, in), s->face, s->stream, 1, tile);
         } else {
             tile[0] = i / s->ks.cell_tc;
             tile[1] = j;
@@ -494,6 +541,8 @@ void collect_times(hgks_solver* s, int stages) {
         cudaEventElapsedTime(&b, s->ev[st * 3 + 1], s->ev[st * 3 + 2]);
         s->t_face += a;
         s->t_cell += b;
+        s->t_stage[st][0] = a;
+        s->t_stage[st][1] = b;
     }
 }
 
@@ -596,7 +645,7 @@ int hgks_create(const hgks_config* cfg, hgks_solver** out) {
     CK(cudaMallocHost(&s->h_stat, 2 * sizeof(StepStatus)));
     CK(cudaMalloc(&s->d_halo, 4 * (size_t)s->S * s->NC * sizeof(double)));
     CK(cudaMemset(s->d_halo, 0, 4 * (size_t)s->S * s->NC * sizeof(double)));
-    return HGKS_OK;
+    return make_qmaps(s);
 }
 
 void hgks_destroy(hgks_solver* s) {
@@ -1110,13 +1159,13 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
         ++s->launches;
         return cudaGetLastError();
     };
-    auto F1 = [&](int c) { K.face_layers(kp1, qn, s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
+    auto F1 = [&](int c) { K.face_layers(kp1, qn, qmap_of(s, qn), s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
     auto C1 = [&](int c) {
         K.cell_layers(kp1, MODE_STAGE1, qn, s->face, nullptr, nullptr, nullptr, s->qs, s->A, nullptr, cs,
                       kb(c), kb(c + 1));
         ++s->launches;
     };
-    auto F2 = [&](int c) { K.face_layers(kp2, s->qs, s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
+    auto F2 = [&](int c) { K.face_layers(kp2, s->qs, qmap_of(s, s->qs), s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
     auto C2 = [&](int c) {
         K.cell_layers(kp2, MODE_STAGE2, s->qs, s->face, nullptr, s->A, nullptr, qnew, nullptr, nullptr, cs,
                       kb(c), kb(c + 1));
@@ -1512,6 +1561,13 @@ int hgks_kernel_times(hgks_solver* s, double* face_ms, double* cell_ms, double* 
     return HGKS_OK;
 }
 
+int hgks_kernel_times_stage(hgks_solver* s, int stage, double* face_ms, double* cell_ms) {
+    if (stage < 0 || stage > 1) return fail(s, HGKS_ERR_CONFIG, "hgks_kernel_times_stage: stage 0 or 1");
+    if (face_ms) *face_ms = s->t_stage[stage][0];
+    if (cell_ms) *cell_ms = s->t_stage[stage][1];
+    return HGKS_OK;
+}
+
 void hgks_set_graphs(hgks_solver* s, int on) {
     if (!on) drop_graphs(s);
     s->use_graphs = on != 0;
@@ -1520,6 +1576,11 @@ void hgks_set_graphs(hgks_solver* s, int on) {
 void hgks_set_grid_cap(hgks_solver* s, int ctas) {
     drop_graphs(s);
     s->grid_cap = ctas > 0 ? ctas : 0;
+}
+
+void hgks_set_face_tma(hgks_solver* s, int on) {
+    drop_graphs(s);
+    s->face_tma = on != 0;
 }
 
 void hgks_set_race_shake(hgks_solver* s, unsigned seed) {

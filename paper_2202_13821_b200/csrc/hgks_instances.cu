@@ -13,6 +13,12 @@
 namespace hgks_dev {
 namespace {
 
+// kernel argument when no tensor map is needed (cp.async staging)
+inline const CUtensorMap& map_or_null(const CUtensorMap* m) {
+    static const CUtensorMap zero{};
+    return m ? *m : zero;
+}
+
 // persistent grid size: resident CTAs on the GPU, optionally capped
 // (KParams::grid_cap, a test hook that makes every CTA walk many tiles)
 inline int capped(const KParams& kp, int g) {
@@ -27,7 +33,7 @@ struct Launch {
     static int face_smem() {
         // staged coefficients of both neighbours (double-buffered by default)
         // [+ the flux accumulators when they live in shared memory]
-        return (HGKS_FACE_STAGES * (2 * SH::NC * 32) +
+        return (HGKS_FACE_STAGES * FaceStage<SH::NC, AXIS>::STG +
                 (HGKS_FACE_ACC_SMEM ? 35 * FaceCTA<P, DIM, AXIS>::NT : 0)) *
                (int)sizeof(double);
     }
@@ -39,7 +45,7 @@ struct Launch {
     static inline int cell_grid[3] = {0, 0, 0};
 
     template <int AXIS>
-    static void face_axis(const KParams& kp, const double* q, double* f, cudaStream_t st,
+    static void face_axis(const KParams& kp, const double* q, const CUtensorMap* qm, double* f, cudaStream_t st,
                           int report, const int* tile) {
         const int layers = AXIS == 2 ? kp.zface_layers : kp.nzl;
         int t[3] = {0, 0, 0};
@@ -59,29 +65,30 @@ struct Launch {
             grid = 1;
         }
         (void)NFP;
-        face_kernel<P, DIM, VISC, AXIS><<<grid, FaceCTA<P, DIM, AXIS>::NT, face_smem<AXIS>(), st>>>(kp, q, f, first, count, 0);
+        face_kernel<P, DIM, VISC, AXIS><<<grid, FaceCTA<P, DIM, AXIS>::NT, face_smem<AXIS>(), st>>>(
+            kp, q, f, first, count, map_or_null(qm ? qm + (AXIS == 0 ? 1 : 0) : nullptr));
     }
     template <int AXIS>
-    static void face_axis_layers(const KParams& kp, const double* q, double* f, cudaStream_t st,
-                                 int kb, int ke) {
+    static void face_axis_layers(const KParams& kp, const double* q, const CUtensorMap* qm, double* f,
+                                 cudaStream_t st, int kb, int ke) {
         const int ntx = (kp.nx + 31) / 32;
         const int first = ntx * kp.ny * kb, count = ntx * kp.ny * (ke - kb);
         if (count <= 0) return;
         const int grid = std::min(count, capped(kp, face_grid[AXIS]));
         face_kernel<P, DIM, VISC, AXIS><<<grid, FaceCTA<P, DIM, AXIS>::NT, face_smem<AXIS>(), st>>>(
-            kp, q, f, first, count, 0);
+            kp, q, f, first, count, map_or_null(qm ? qm + (AXIS == 0 ? 1 : 0) : nullptr));
     }
-    static void face_axis_range(const KParams& kp, int axis, const double* q, double* f, cudaStream_t st,
-                                int kb, int ke) {
-        if (axis == 0) face_axis_layers<0>(kp, q, f, st, kb, ke);
-        else if (axis == 1) face_axis_layers<1>(kp, q, f, st, kb, ke);
-        else face_axis_layers<2>(kp, q, f, st, kb, ke);
+    static void face_axis_range(const KParams& kp, int axis, const double* q, const CUtensorMap* qm, double* f,
+                                cudaStream_t st, int kb, int ke) {
+        if (axis == 0) face_axis_layers<0>(kp, q, qm, f, st, kb, ke);
+        else if (axis == 1) face_axis_layers<1>(kp, q, qm, f, st, kb, ke);
+        else face_axis_layers<2>(kp, q, qm, f, st, kb, ke);
     }
-    static void face_layers(const KParams& kp, const double* q, double* const f[3], cudaStream_t st,
-                            int kb, int ke) {
-        face_axis_layers<0>(kp, q, f[0], st, kb, ke);
-        face_axis_layers<1>(kp, q, f[1], st, kb, ke);
-        face_axis_layers<2>(kp, q, f[2], st, kb, ke);
+    static void face_layers(const KParams& kp, const double* q, const CUtensorMap* qm, double* const f[3],
+                            cudaStream_t st, int kb, int ke) {
+        face_axis_layers<0>(kp, q, qm, f[0], st, kb, ke);
+        face_axis_layers<1>(kp, q, qm, f[1], st, kb, ke);
+        face_axis_layers<2>(kp, q, qm, f[2], st, kb, ke);
     }
     static void cell_layers(const KParams& kp, int mode, const double* qin, double* const f[3],
                             const double* qn, const double* L1, const double* Lt1, double* o0,
@@ -99,12 +106,12 @@ struct Launch {
                                                      cell_smem<MODE_STAGE2>(), st>>>(
                 kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
     }
-    static void face(const KParams& kp, const double* q, double* const f[3], cudaStream_t st,
+    static void face(const KParams& kp, const double* q, const CUtensorMap* qm, double* const f[3], cudaStream_t st,
                      int report, const int* tile) {
         // report mode re-runs only the failing axis' tile (tile[3] = axis)
-        if (!report || tile[3] == 0) face_axis<0>(kp, q, f[0], st, report, tile);
-        if (!report || tile[3] == 1) face_axis<1>(kp, q, f[1], st, report, tile);
-        if (!report || tile[3] == 2) face_axis<2>(kp, q, f[2], st, report, tile);
+        if (!report || tile[3] == 0) face_axis<0>(kp, q, qm, f[0], st, report, tile);
+        if (!report || tile[3] == 1) face_axis<1>(kp, q, qm, f[1], st, report, tile);
+        if (!report || tile[3] == 2) face_axis<2>(kp, q, qm, f[2], st, report, tile);
     }
     static void cell(const KParams& kp, int mode, const double* qin, double* const f[3],
                      const double* qn, const double* L1, const double* Lt1, double* o0, double* o1,
@@ -182,6 +189,7 @@ struct Launch {
         k.face_smem[2] = face_smem<2>();
         k.cell_smem = cell_smem();
         k.cell_tc = SH::TC;
+        k.face_tma = HGKS_FACE_STAGES == 2;  // the TMA path needs the double-buffered stage
         k.nfp[0] = SH::template nfp<0>();
         k.nfp[1] = SH::template nfp<1>();
         k.nfp[2] = SH::template nfp<2>();

@@ -13,6 +13,7 @@
 // Basis/quadrature values are compile-time constants (hgks_ctables.cuh).
 #pragma once
 
+#include <cuda.h>
 #include <stdint.h>
 
 #include "hgks_ctables.cuh"
@@ -43,10 +44,18 @@
 #ifndef HGKS_FACE_ACC_SMEM
 #define HGKS_FACE_ACC_SMEM 0
 #endif
+// face kernel staging: both paths are compiled; KParams::face_tma selects
+// TMA (cp.async.bulk.tensor of the two neighbour [NC][32] boxes per tile,
+// one elected thread, mbarrier completion) or per-lane cp.async at run time
 // threads of the 3-D P1/P2 cell kernel (0: one per (cell, volume point));
 // 160 = one per (cell, var, F|Ft) item of the stage-1 projection, 10 warps/SM
 #ifndef HGKS_CELL_NT3
 #define HGKS_CELL_NT3 160
+#endif
+// cell kernel: end-of-tile barrier before the next tile's face prefetch (1)
+// or face / coefficient prefetch issued after the top barrier (0)
+#ifndef HGKS_CELL_ENDBAR
+#define HGKS_CELL_ENDBAR 0
 #endif
 // cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
 #ifndef HGKS_CELL_TC
@@ -104,6 +113,7 @@ struct KParams {
     double two_mu;         // 2 mu: face tau = 2 mu / (p_l + p_r)
     int grid_cap;          // > 0: cap on the persistent grids (tests: many tiles per CTA)
     unsigned shake;        // != 0: race shaker seed (tests; see race_shake)
+    int face_tma;          // 1: face kernels stage by TMA (the qmap argument is valid)
     GasC gas;
     const double* dx;      // [nx] widths
     const double* dy;      // [ny]
@@ -350,6 +360,48 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// ---- TMA (cp.async.bulk.tensor) + mbarrier helpers
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+// one [box] of a 3-D tensor map (x, row, comp) into shared memory, completing
+// on `bar` (transaction bytes)
+__device__ __forceinline__ void tma_load3(double* dst, const CUtensorMap* map, int x, int row, int comp,
+                                          uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+            (unsigned)__cvta_generic_to_shared(dst)),
+        "l"(map), "r"(x), "r"(row), "r"(comp), "r"((unsigned)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+
+// face-kernel stage layout: y / z faces [side][comp][32]; x faces one shared
+// [comp][34] row (x = i0-2 .. i0+31), minus side at column lane+1, plus side
+// at lane+2
+template <int NC, int AXIS>
+struct FaceStage {
+    // stages start 128-byte aligned (TMA destinations)
+    static constexpr int STG = AXIS == 0 ? (34 * NC + 15) / 16 * 16 : 2 * NC * 32;
+    static constexpr int RSL = AXIS == 0 ? 34 : 32, RSR = RSL;
+    static constexpr int OFL = AXIS == 0 ? 1 : 0, OFR = AXIS == 0 ? 2 : NC * 32;
+};
+
 // Persistent face kernel. A CTA = NFP warps; each tile is 32 consecutive faces
 // along x (one lane each) at one (j, k), one face point per warp, so the
 // point index is warp-uniform. The two neighbour cells' coefficients of the
@@ -367,15 +419,20 @@ struct FaceCTA {
 template <int P, int DIM, bool VISC, int AXIS>
 __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P, VISC))
     face_kernel(KParams kp, const double* __restrict__ q, double* __restrict__ face,
-                int tile_first, int tile_count, int unused) {
+                int tile_first, int tile_count, const __grid_constant__ CUtensorMap qmap) {
     using SH = Shape<P, DIM>;
     constexpr int NC = SH::NC;
     constexpr int NFP = SH::template nfp<AXIS>();
     constexpr int PPW = FaceCTA<P, DIM, AXIS>::PPW;
     constexpr int NT = FaceCTA<P, DIM, AXIS>::NT;
     constexpr int C1 = (AXIS + 1) % 3, C2 = (AXIS + 2) % 3;
-    constexpr int STG = 2 * NC * 32;  // one stage: [side][comp][32]
-    extern __shared__ double smem[];
+    // one stage: y / z faces [side][comp][32]; x faces ONE [comp][34] row
+    // (x = i0-2 .. i0+31): the minus neighbour of lane l is column l+1, the
+    // plus neighbour column l+2 (the two sides overlap in x)
+    constexpr int STG = FaceStage<NC, AXIS>::STG;
+    constexpr int RSL = FaceStage<NC, AXIS>::RSL, RSR = FaceStage<NC, AXIS>::RSR;
+    constexpr int OFL = FaceStage<NC, AXIS>::OFL, OFR = FaceStage<NC, AXIS>::OFR;
+    extern __shared__ __align__(128) double smem[];  // 128 B: TMA destinations
 
     if (kp.scal[SC_ACTIVE] == 0.0) return;  // halted device loop: no-op step
     const double inv_dt = kp.scal[SC_INV_DT], rh_coef = kp.scal[SC_RH];
@@ -393,16 +450,31 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
     // both neighbours' coefficients of one tile: lane = face, rows = components
     // (each warp streams its share of the 2*NC rows, 256 B per row)
     auto prefetch = [&](const TI& ti, double* dst) {
+        constexpr int NW = NT / 32;
+        if (AXIS == 0) {
+            // columns 0..33 = x = i0-2 .. i0+31 (periodic wrap at both ends;
+            // lanes 0, 1 also fetch columns 32, 33)
+            const long row = (long)(ti.k + 1) * kp.S + (long)ti.j * nx;
+            auto xw = [&](int x) { return x < 0 ? x + nx : x >= nx ? x - nx : x; };
+            const int xa = ti.i0 - 2 + lane, xb = ti.i0 + 30 + lane;
+            const bool oka = xa < nx, okb = lane < 2 && xb < nx;
+            const double* sa = q + row + (oka ? xw(xa) : 0);
+            const double* sb = q + row + (okb ? xw(xb) : 0);
+#pragma unroll 4
+            for (int c = warp; c < NC; c += NW) {
+                cp_async8(dst + c * 34 + lane, sa + c * kp.cs, oka);
+                if (lane < 2) cp_async8(dst + c * 34 + 32 + lane, sb + c * kp.cs, okb);
+            }
+            return;
+        }
         const int i = ti.i0 + lane;
         const bool ok = i < nx;
         const int ci = ok ? i : 0;
-        int mi = ci, mj = ti.j, mk = ti.k;
-        if (AXIS == 0) mi = ci == 0 ? nx - 1 : ci - 1;
+        int mj = ti.j, mk = ti.k;
         if (AXIS == 1) mj = ti.j == 0 ? ny - 1 : ti.j - 1;
         if (AXIS == 2) mk = ti.k - 1;
-        const double* sL = q + (long)(mk + 1) * kp.S + (long)mj * nx + mi;
+        const double* sL = q + (long)(mk + 1) * kp.S + (long)mj * nx + ci;
         const double* sR = q + (long)(ti.k + 1) * kp.S + (long)ti.j * nx + ci;
-        constexpr int NW = NT / 32;
 #pragma unroll 4
         for (int c = warp; c < NC; c += NW) {
             cp_async8(dst + c * 32 + lane, sL + c * kp.cs, ok);
@@ -410,25 +482,74 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
         }
     };
 
+    // TMA staging: both neighbours' [NC][32] boxes of a tile, one elected
+    // thread, completion counted in bytes on the stage's mbarrier
+    __shared__ uint64_t mbar[2];
+    const bool tma = kp.face_tma != 0 && HGKS_FACE_STAGES == 2;
+    // (the box start must be 16-byte aligned: x starts at even columns)
+    auto tma_tile = [&](const TI& ti, int stage) {
+        double* dst = smem + stage * STG;
+        const int rowR = ti.j + ny * (ti.k + 1);
+        if (AXIS == 0) {
+            // one 34-wide box from x = i0-2 (x < 0 at i0 = 0 is zero-filled
+            // and patched after the wait: TMA has no periodic wrap)
+            mbar_expect_tx(&mbar[stage], 34u * NC * 8u);
+            tma_load3(dst, &qmap, ti.i0 - 2, rowR, 0, &mbar[stage]);
+            return;
+        }
+        const int rowL = AXIS == 1 ? (ti.j == 0 ? ny - 1 : ti.j - 1) + ny * (ti.k + 1) : ti.j + ny * ti.k;
+        mbar_expect_tx(&mbar[stage], 2u * NC * 32u * 8u);
+        tma_load3(dst, &qmap, ti.i0, rowL, 0, &mbar[stage]);
+        tma_load3(dst + NC * 32, &qmap, ti.i0, rowR, 0, &mbar[stage]);
+    };
+    if (tma) {
+        if (tid == 0) {
+            mbar_init(&mbar[0], 1);
+            mbar_init(&mbar[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+    }
     const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
     TI cur = walk.of(t0);
-    if (t0 < tile_end) prefetch(cur, smem);
-    cp_async_commit();
+    if (tma) {
+        if (tid == 0 && t0 < tile_end) tma_tile(cur, 0);
+    } else {
+        if (t0 < tile_end) prefetch(cur, smem);
+        cp_async_commit();
+    }
     int n = 0;
     for (int t = t0; t < tile_end; t += step, ++n) {
         double* sc = smem + (HGKS_FACE_STAGES == 2 ? (n & 1) * STG : 0);
         const bool has_next = t + step < tile_end;
         const TI nxt = walk.next(cur);
-        if (HGKS_FACE_STAGES == 2) {
+        if (tma) {
+            if (tid == 0 && has_next) {
+                // the other stage was last read in tile n-1 (end-of-tile barrier)
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                tma_tile(nxt, (n + 1) & 1);
+            }
+        } else if (HGKS_FACE_STAGES == 2) {
             if (has_next) prefetch(nxt, smem + ((n + 1) & 1) * STG);
             cp_async_commit();
         }
         const int i0 = cur.i0, j = cur.j, k = cur.k;
         const int i = i0 + lane;
         race_shake(kp, 0, n);
-        if (HGKS_FACE_STAGES == 2) cp_async_wait<1>();  // this tile's stage
-        else cp_async_wait<0>();
-        __syncthreads();
+        if (tma) {
+            mbar_wait(&mbar[n & 1], (n >> 1) & 1);  // this tile's stage landed
+            if (AXIS == 0 && i0 == 0) {
+                // periodic x: the minus neighbour of face 0 is cell nx-1 (TMA
+                // has no wrap; column 1 = x = -1 arrived zero-filled)
+                const double* src = q + (long)(k + 1) * kp.S + (long)j * nx + (nx - 1);
+                for (int c = tid; c < NC; c += NT) sc[c * 34 + 1] = __ldg(src + c * kp.cs);
+                __syncthreads();
+            }
+        } else {
+            if (HGKS_FACE_STAGES == 2) cp_async_wait<1>();  // this tile's stage
+            else cp_async_wait<0>();
+            __syncthreads();
+        }
 #pragma unroll 1
         for (int ip = 0; ip < PPW; ++ip) {
         const int p = warp * PPW + ip;
@@ -438,8 +559,8 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
             const int km = AXIS == 2 ? k - 1 : k;
             const double i2hL[3] = {__ldg(kp.i2dx + im), __ldg(kp.i2dy + jm), __ldg(kp.i2dz + km + 1)};
             const double i2hR[3] = {__ldg(kp.i2dx + i), __ldg(kp.i2dy + j), __ldg(kp.i2dz + k + 1)};
-            const double* cL = sc + lane;
-            const double* cR = sc + NC * 32 + lane;
+            const double* cL = sc + OFL + lane;
+            const double* cR = sc + OFR + lane;
 
 #if HGKS_FACE_ACC_SMEM
             SmemAcc acc{smem + HGKS_FACE_STAGES * STG + tid, NT};
@@ -462,8 +583,8 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
 #pragma unroll
             for (int side = 0; side < 2; ++side) {
                 double tr[20];
-                if (side == 0) face_trace_sym<P, DIM, AXIS, 0, 32>(p, cL, i2hL, tr);
-                else face_trace_sym<P, DIM, AXIS, 1, 32>(p, cR, i2hR, tr);
+                if (side == 0) face_trace_sym<P, DIM, AXIS, 0, RSL>(p, cL, i2hL, tr);
+                else face_trace_sym<P, DIM, AXIS, 1, RSR>(p, cR, i2hR, tr);
                 double ps = 0.0;
                 rcs[side] = flux_side<VISC>(tr, side, kp.gas, acc, ps, bads[side]);
                 psum += ps;
@@ -487,8 +608,8 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
 #pragma unroll 1
             for (int side = 0; side < 2 && !fail; ++side) {
                 double tr[20];
-                if (side == 0) face_trace_sym<P, DIM, AXIS, 0, 32>(p, cL, i2hL, tr);
-                else face_trace_sym<P, DIM, AXIS, 1, 32>(p, cR, i2hR, tr);
+                if (side == 0) face_trace_sym<P, DIM, AXIS, 0, RSL>(p, cL, i2hL, tr);
+                else face_trace_sym<P, DIM, AXIS, 1, RSR>(p, cR, i2hR, tr);
                 double bad = 0.0, ps = 0.0;
                 const int rc = flux_side<VISC>(tr, side, kp.gas, acc, ps, bad);
                 psum += ps;
@@ -542,7 +663,7 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
         }
         cur = nxt;
     }
-    cp_async_wait<0>();
+    if (!tma) cp_async_wait<0>();
 }
 
 // -------------------------------------------------------------- cell kernel
@@ -641,7 +762,7 @@ enum : int { MODE_RESIDUAL = 0, MODE_STAGE1 = 1, MODE_STAGE2 = 2 };
 template <int P, int DIM, int MODE>
 struct CellTile {
     using SH = Shape<P, DIM>;
-    static constexpr int TC = SH::TC, NC = SH::NC, NVP = SH::NVP, N = SH::N;
+    static constexpr int TC = SH::TC, NC = SH::NC, NVP = SH::NVP;
     static constexpr int NFX = SH::template nfp<0>(), NFY = SH::template nfp<1>(),
                          NFZ = SH::template nfp<2>();
     static constexpr int RW = MODE == MODE_STAGE2 ? 5 : 10, RO = 10 - RW;
@@ -651,43 +772,25 @@ struct CellTile {
     static constexpr int FZ = NFZ * RW * 2 * TC;   // z faces layers k, k+1
     static constexpr int VFW = 3 * RW;             // flux rows per volume point
     static constexpr int VF = NVP * VFW * TC;      // volume-point fluxes [p][VFW][TC]
+    static constexpr int LB = MODE == MODE_STAGE1 ? 2 * NC * TC : 0;  // L, Lt of the tile (stage-1 q*)
     static constexpr int GEO = 2 * TC + 4;          // widths of a tile: dx, 2/dx [TC]; dy, dz, 2/dy, 2/dz
     // stage 2: the tile's A = q + dt L1 + dt^2/6 Lt1 [NC][TC], prefetched with the faces
     static constexpr int AB = MODE == MODE_STAGE2 ? COEF : 0;
+    static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + LB + 2 * GEO + AB;
     // threads / resident CTAs: stage 2 (half the tile, ~150 registers) runs
     // one thread per (cell, volume point) at 3 CTAs per SM for 3-D P1/P2
     static constexpr bool S2X = MODE == MODE_STAGE2 && P < 3 && DIM == 3;
     static constexpr int NT = S2X ? TC * NVP : SH::NT_CELL;
     static constexpr int MINB = S2X ? 3 : SH::MINB_CELL;
-    // projection items (cell, var, F|Ft); stage 2 projects only Ft
-    static constexpr int NITEMS = TC * 5 * (MODE == MODE_STAGE2 ? 1 : 2);
-    // phase B occupies the first NBT threads; when whole warps are left over
-    // (3-D P1/P2, 160 threads: warp 4) they are the FACE warps: they fetch the
-    // tile's face fluxes themselves and reduce the face part of every
-    // projection item while phase B runs (the cell kernel's idle warp of
-    // phase B in the one-phase-at-a-time design)
-    static constexpr int NBT = ((TC * NVP + 31) / 32) * 32;
-    static constexpr bool FCW = NT - NBT >= 32;
-    static constexpr int RF = FCW ? N * NITEMS : 0;  // face parts of the items [m][item]
-    static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + RF + 2 * GEO + AB;
 };
 
 // Persistent CTA over tiles of TC consecutive cells along x, software
-// pipelined with TWO CTA barriers per tile:
-//   top:  the tile's coefficients / widths (prefetched a tile ahead) landed
-//         -> barrier -> issue this tile's face fluxes (+ stage 2's A tile)
-//         and the next tile's coefficients
-//   phase B (threads < NBT): one (cell, volume point) item per thread ->
-//         smooth fluxes at the volume points (vf)
-//   face warps (FCW): meanwhile the face part of every projection item
-//         (+ w jac B- F(minus) - w jac B+ F(plus)) into rf
-//   barrier (vf, rf / the faces complete)
-//   phase C: one (cell, var, F|Ft) item per thread -> volume projection,
-//         M^-1 and the fused S2O4 combine; the F and Ft items of a (cell,
-//         var) sit in adjacent lanes and swap L / Lt with one shuffle, so
-//         stage 1 writes q* (F lane) and A (Ft lane) with no barrier.
-// Nothing a tile writes in shared memory is read after the next top barrier,
-// so no end-of-tile barrier is needed.
+// pipelined: while tile t is computed, the coefficients of tile t+grid and
+// the face fluxes of tile t stream into shared memory (cp.async).
+// Phase B: one (cell, volume point) item per thread -> smooth fluxes.
+// Phase C: one (cell, var, F|Ft) item per thread -> face gather + volume
+// projection + M^-1 (+ S2O4 combine); stage 1 then forms q* per coefficient
+// from shared memory, stage 2 needs only Lt2.
 template <int P, int DIM, bool VISC, int MODE>
 __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, MODE>::MINB)
     cell_kernel(KParams kp, const double* __restrict__ qin, const double* __restrict__ f0,
@@ -699,16 +802,15 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
     using SH = Shape<P, DIM>;
     using CT = CellTile<P, DIM, MODE>;
     constexpr int N = SH::N, NC = SH::NC, NVP = SH::NVP, TC = SH::TC;
-    constexpr int NT = CT::NT, NAX = SH::NAX, NITEMS = CT::NITEMS, NBT = CT::NBT;
-    constexpr bool FCW = CT::FCW;
-    extern __shared__ double smem[];
+    constexpr int NT = CT::NT, NAX = SH::NAX;
+    extern __shared__ __align__(128) double smem[];  // 128 B: TMA destinations
     double* coefb = smem;                 // [2][NC][TC]
     double* fx = coefb + 2 * CT::COEF;
     double* fy = fx + CT::FX;
     double* fz = fy + CT::FY;
     double* vf = fz + CT::FZ;             // [NVP][VFW][TC]
-    double* rf = vf + CT::VF;             // [N][NITEMS] face parts (FCW)
-    double* geob = rf + CT::RF;           // [2][GEO], staged with the coefficients
+    double* lb = vf + CT::VF;             // [2][NC][TC]
+    double* geob = lb + CT::LB;           // [2][GEO], staged with the coefficients
     double* ab = geob + 2 * CT::GEO;      // [NC][TC] stage 2: A of the tile
 
     const int tid = threadIdx.x;
@@ -758,10 +860,8 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
     // stage 2 consumes only the Ft rows (the face pass stores only those)
     constexpr int RW = CT::RW, RO = CT::RO;
     auto face_row = [](int rr) { return (rr / RW) * 10 + RO + rr % RW; };
-    // the tile's face fluxes, issued by threads [t0, t0 + nthr) (the face
-    // warps on the FCW path, else every thread)
-    auto prefetch_faces = [&](const TI& ti, int t0, int nthr) {
-        const int ltid = tid - t0;
+    auto prefetch_faces = [&](const TI& ti) {
+        if (MODE == MODE_STAGE2) prefetch_state(L1, ti, ab);
         const int i0 = ti.i0, j = ti.j, k = ti.k;
         const long rowk = (long)nx * (j + (long)ny * k);
         const int jp = j + 1 == ny ? 0 : j + 1;
@@ -771,8 +871,8 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
         if constexpr (2 * TC == 32) {
             // one face row per warp instruction: x rows hold TC+1 faces
             // (lanes 0..TC), y/z rows the TC faces of both neighbour rows
-            const int NW = nthr / 32;
-            const int lane = ltid & 31, warp = ltid >> 5;
+            constexpr int NW = NT / 32;
+            const int lane = tid & 31, warp = tid >> 5;
             const int igx = i0 + lane;
             const bool okx = lane <= TC && igx <= nx;  // x is periodic: face nx is face 0
             const long ox = rowk + (okx ? (igx == nx ? 0 : igx) : 0);
@@ -799,20 +899,20 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
                     cp_async8(fz + (pf * RW + c) * 2 * TC + lane, sz + pf * pst, ok);
             }
         } else {
-            for (int e = ltid; e < CT::NFX * RW * (TC + 1); e += nthr) {  // x faces i0 .. i0+TC (periodic wrap at nx)
+            for (int e = tid; e < CT::NFX * RW * (TC + 1); e += NT) {  // x faces i0 .. i0+TC (periodic wrap at nx)
                 const int l = e % (TC + 1), r = face_row(e / (TC + 1));
                 const int ig = i0 + l;
                 const bool ok = ig <= nx;  // x is always periodic: face nx is face 0
                 const int iw = ig == nx ? 0 : ig;
                 cp_async8(fx + e, f0 + (long)r * kp.fs + rowk + (ok ? iw : 0), ok);
             }
-            for (int e = ltid; e < CT::NFY * RW * 2 * TC; e += nthr) {  // y faces of rows j, j+1
+            for (int e = tid; e < CT::NFY * RW * 2 * TC; e += NT) {  // y faces of rows j, j+1
                 const int l = e % (2 * TC), r = face_row(e / (2 * TC));
                 const int ig = i0 + (l % TC);
                 const bool ok = ig < nx;
                 cp_async8(fy + e, f1 + (long)r * kp.fs + (l < TC ? rowk : rowp) + (ok ? ig : 0), ok);
             }
-            for (int e = ltid; e < CT::NFZ * RW * 2 * TC; e += nthr) {  // z faces of layers k, k+1
+            for (int e = tid; e < CT::NFZ * RW * 2 * TC; e += NT) {  // z faces of layers k, k+1
                 const int l = e % (2 * TC), r = face_row(e / (2 * TC));
                 const int ig = i0 + (l % TC);
                 const bool ok = ig < nx;
@@ -820,60 +920,6 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
             }
         }
     };
-    // projection item -> (cell column l, variable v, F (0) | Ft (1)); the F
-    // and Ft items of a (cell, var) are adjacent lanes (stage 1 / residual)
-    auto item_of = [](int it, int& l, int& v, int& ft) {
-        if (MODE == MODE_STAGE2) {
-            ft = 1;
-            l = it % TC;
-            v = it / TC;
-        } else {
-            ft = it & 1;
-            l = (it >> 1) % TC;
-            v = (it >> 1) / TC;
-        }
-    };
-    // face part of item it (dg.hpp:404-425): + w jac B- F(minus face) - w jac
-    // B+ F(plus face), with the Legendre parity B+(p,n) = (-1)^{n_a} B-(p,n)
-    auto face_part = [&](int it, const double* gg, double hy, double hz, double* R) {
-        int l, v, ft;
-        item_of(it, l, v, ft);
-        const int row = 5 * ft + v;
-        const double hx = gg[l];
-        const double jac[3] = {hy * hz * 0.25, hz * hx * 0.25, hx * hy * 0.25};
-#pragma unroll
-        for (int m = 0; m < N; ++m) R[m] = 0.0;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const int nfp = a == 0 ? CT::NFX : a == 1 ? CT::NFY : CT::NFZ;
-            double acc[N];
-#pragma unroll
-            for (int m = 0; m < N; ++m) acc[m] = 0.0;
-#pragma unroll
-            for (int pf = 0; pf < nfp; ++pf) {
-                const int r = pf * RW + row - RO;
-                double Fm, Fp;
-                if (a == 0) {
-                    Fm = fx[r * (TC + 1) + l];
-                    Fp = fx[r * (TC + 1) + l + 1];
-                } else {
-                    const double* fa = a == 1 ? fy : fz;
-                    Fm = fa[r * 2 * TC + l];
-                    Fp = fa[r * 2 * TC + TC + l];
-                }
-                const double Dm = Fm - Fp, Sm = Fm + Fp;
-#pragma unroll
-                for (int m = 0; m < N; ++m) {
-                    const double c = ctab<P, DIM>.fw[a][pf] * ctab<P, DIM>.fB[a][0][pf][m];
-                    const bool odd = ctab<P, DIM>.par[a][m] != 0;
-                    if (c != 0.0) acc[m] += c * (odd ? Sm : Dm);
-                }
-            }
-#pragma unroll
-            for (int m = 0; m < N; ++m) R[m] += jac[a] * acc[m];
-        }
-    };
-
     if (kp.scal[SC_ACTIVE] == 0.0) return;  // halted device loop: no-op step
     const double dt = kp.scal[SC_DT];
     const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
@@ -885,81 +931,105 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
         double* sc = coefb + (n & 1) * CT::COEF;
         const bool has_next = t + step < tile_end;
         const TI nxt = walk.next(cur);
+#if HGKS_CELL_ENDBAR
+        prefetch_faces(cur);
+        cp_async_commit();
+        if (has_next) prefetch_coef(nxt, coefb + ((n + 1) & 1) * CT::COEF, geob + ((n + 1) & 1) * CT::GEO);
+        cp_async_commit();
+#endif
         const int i0 = cur.i0, j = cur.j, k = cur.k;
         const long cbase = (long)(k + 1) * kp.S + (long)j * nx;
         const double* gg = geob + (n & 1) * CT::GEO;
         const long cglob_row = (long)nx * (j + (long)ny * (k + kp.kglob0));
         race_shake(kp, 2, n);
-        cp_async_wait<0>();  // this tile's coefficients and widths (issued a tile ahead)
-        __syncthreads();     // ... visible to all; the previous tile's buffers are free
-        // face fluxes of this tile (+ stage 2's A tile), then the next tile's
-        // coefficients; the face warps fetch their own faces
-        if (MODE == MODE_STAGE2) prefetch_state(L1, cur, ab);
-        if (!FCW) prefetch_faces(cur, 0, NT);
-        else if (tid >= NBT) prefetch_faces(cur, NBT, NT - NBT);
+#if HGKS_CELL_ENDBAR
+        cp_async_wait<2>();  // this tile's coefficients and widths
+        __syncthreads();
+#else
+        // one barrier less per tile: the tile's faces and the next tile's
+        // coefficients are issued after this barrier, when every buffer the
+        // previous tile read is free
+        cp_async_wait<0>();  // this tile's coefficients and widths
+        __syncthreads();
+        prefetch_faces(cur);
         cp_async_commit();
         if (has_next) prefetch_coef(nxt, coefb + ((n + 1) & 1) * CT::COEF, geob + ((n + 1) & 1) * CT::GEO);
         cp_async_commit();
+#endif
         const double hy = gg[2 * TC], hz = gg[2 * TC + 1];
         const double i2hy = gg[2 * TC + 2], i2hz = gg[2 * TC + 3];
 
-        if (!FCW || tid < NBT) {
-            // ---- phase B: smooth fluxes at volume points
-            for (int it = tid; it < TC * NVP; it += (FCW ? NBT : NT)) {
-                const int l = it % TC;
-                const int p = SH::NQ == 2 ? it / TC : kVolOrder<P, DIM>.p[it / TC];
-                const int i = i0 + l;
-                if (i >= nx) continue;
-                const double i2h[3] = {gg[TC + l], i2hy, i2hz};
-                double e[20];
-                vol_eval_sym<P, DIM, TC>(p, sc + l, i2h, e);
-                double o[30];
-                double bad = 0.0;
-                const int rc = smooth_flux<VISC, NAX, MODE == MODE_STAGE2>(e, kp.gas, o, bad);
-                if (rc) {
-                    report_error(kp, err_key(kp.stage, 1, cglob_row + i, p, 0, rc), bad);
+        // ---- phase B: smooth fluxes at volume points
+        for (int it = tid; it < TC * NVP; it += NT) {
+            const int l = it % TC;
+            const int p = SH::NQ == 2 ? it / TC : kVolOrder<P, DIM>.p[it / TC];
+            const int i = i0 + l;
+            if (i >= nx) continue;
+            const double i2h[3] = {gg[TC + l], i2hy, i2hz};
+            double e[20];
+            vol_eval_sym<P, DIM, TC>(p, sc + l, i2h, e);
+            double o[30];
+            double bad = 0.0;
+            const int rc = smooth_flux<VISC, NAX, MODE == MODE_STAGE2>(e, kp.gas, o, bad);
+            if (rc) {
+                report_error(kp, err_key(kp.stage, 1, cglob_row + i, p, 0, rc), bad);
 #pragma unroll
-                    for (int m = 0; m < 30; ++m) o[m] = 0.0;
-                }
-#pragma unroll
-                for (int m = 0; m < 10 * NAX; ++m)
-                    if (m % 10 >= RO) vf[(p * CT::VFW + (m / 10) * RW + m % 10 - RO) * TC + l] = o[m];
+                for (int m = 0; m < 30; ++m) o[m] = 0.0;
             }
-        } else if constexpr (FCW) {
-            // ---- face warps: the face part of every projection item
-            if (!kp.report) {
-                cp_async_wait<1>();  // their own face copies (the coefficient group may still fly)
-                __syncwarp();
-                for (int it = tid - NBT; it < NITEMS; it += NT - NBT) {
-                    double R[N];
-                    face_part(it, gg, hy, hz, R);
 #pragma unroll
-                    for (int m = 0; m < N; ++m) rf[m * NITEMS + it] = R[m];
-                }
-            }
+            for (int m = 0; m < 10 * NAX; ++m)
+                if (m % 10 >= RO) vf[(p * CT::VFW + (m / 10) * RW + m % 10 - RO) * TC + l] = o[m];
         }
         if (kp.report) return;
         race_shake(kp, 3, n);
-        if (!FCW) cp_async_wait<1>();  // this tile's face fluxes
+        cp_async_wait<1>();  // this tile's face fluxes
         __syncthreads();
 
-        // ---- phase C: volume projection + face part + inverse mass (+ combine)
-        for (int it0 = 0; it0 < NITEMS; it0 += NT) {
-            const int it = it0 + tid;
-            if (it >= NITEMS) break;
-            int l, v, ft;
-            item_of(it, l, v, ft);
+        // ---- phase C: gather + projection + inverse mass (+ stage-2 combine)
+        constexpr int FT0 = MODE == MODE_STAGE2 ? 1 : 0;
+        constexpr int NITEMS = TC * 5 * (2 - FT0);
+        for (int it = tid; it < NITEMS; it += NT) {
+            const int l = it % TC, vv = it / TC;
+            const int v = vv % 5, ft = FT0 + vv / 5;  // ft: 0 -> F (R), 1 -> Ft (Rt)
             const int i = i0 + l;
-            const bool valid = i < nx;
+            if (i >= nx) continue;
             const double hx = gg[l];
             const double i2h[3] = {gg[TC + l], i2hy, i2hz};
             const int row = 5 * ft + v;
             double R[N];
-            if constexpr (FCW) {
 #pragma unroll
-                for (int m = 0; m < N; ++m) R[m] = rf[m * NITEMS + it];
-            } else {
-                face_part(it, gg, hy, hz, R);
+            for (int m = 0; m < N; ++m) R[m] = 0.0;
+            // faces (dg.hpp:404-425): + w jac B- F(minus face) - w jac B+ F(plus face),
+            // with the Legendre parity B+(p,n) = (-1)^{n_a} B-(p,n)
+            const double jac[3] = {hy * hz * 0.25, hz * hx * 0.25, hx * hy * 0.25};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int nfp = a == 0 ? CT::NFX : a == 1 ? CT::NFY : CT::NFZ;
+                double acc[N];
+#pragma unroll
+                for (int m = 0; m < N; ++m) acc[m] = 0.0;
+#pragma unroll
+                for (int pf = 0; pf < nfp; ++pf) {
+                    const int r = pf * RW + row - RO;
+                    double Fm, Fp;
+                    if (a == 0) {
+                        Fm = fx[r * (TC + 1) + l];
+                        Fp = fx[r * (TC + 1) + l + 1];
+                    } else {
+                        const double* fa = a == 1 ? fy : fz;
+                        Fm = fa[r * 2 * TC + l];
+                        Fp = fa[r * 2 * TC + TC + l];
+                    }
+                    const double Dm = Fm - Fp, Sm = Fm + Fp;
+#pragma unroll
+                    for (int m = 0; m < N; ++m) {
+                        const double c = ctab<P, DIM>.fw[a][pf] * ctab<P, DIM>.fB[a][0][pf][m];
+                        const bool odd = ctab<P, DIM>.par[a][m] != 0;
+                        if (c != 0.0) acc[m] += c * (odd ? Sm : Dm);
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < N; ++m) R[m] += jac[a] * acc[m];
             }
             // volume (dg.hpp:427-448): + w (h0 h1 h2 / 8) (2/h_a) dB_a F_a
             const double vol = hx * hy * hz;
@@ -985,42 +1055,50 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
             const long g0 = (long)v * kp.cs + cbase + i;
             if (MODE == MODE_RESIDUAL) {
                 double* o = ft ? out1 : out0;
-                if (valid) {
 #pragma unroll
-                    for (int m = 0; m < N; ++m) o[g0 + (long)(m * 5) * kp.cs] = R[m];
-                }
+                for (int m = 0; m < N; ++m) o[g0 + (long)(m * 5) * kp.cs] = R[m];
             } else {
                 // mass_diag (dg.hpp:42-50): 1/M_n = (2nx+1)(2ny+1)(2nz+1)/vol (solver.hpp:49-51)
                 const double ivol = 1.0 / vol;
                 const double c6 = dt * dt / 6.0;
-                if (MODE == MODE_STAGE1) {
-                    // the partner lane holds the other of (L1, Lt1) of this (cell, var):
-                    //   q* = q + dt/2 L1 + dt^2/8 Lt1   (F lane -> out0)
-                    //   A  = q + (dt L1 + dt^2/6 Lt1)   (Ft lane -> out1; stage 2 adds dt^2/6 * 2 Lt2)
-                    // lanes of this warp holding an item (pairs never straddle it)
-                    const int wl = it0 + (tid & ~31);
-                    const unsigned mask = wl + 32 <= NITEMS ? 0xffffffffu : (1u << (NITEMS - wl)) - 1u;
 #pragma unroll
-                    for (int m = 0; m < N; ++m) {
-                        const double L = R[m] * (ctab<P, DIM>.massf[m] * ivol);
-                        const double Lo = __shfl_xor_sync(mask, L, 1);
-                        const double q = sc[(m * 5 + v) * TC + l];
-                        const double Lf = ft ? Lo : L, Lt = ft ? L : Lo;
-                        const double val = ft ? q + (dt * Lf + c6 * Lt) : q + 0.5 * dt * Lf + 0.125 * dt * dt * Lt;
-                        double* o = ft ? out1 : out0;
-                        if (valid) o[g0 + (long)(m * 5) * kp.cs] = val;
-                    }
-                } else {
-                    // q^{n+1} = q + dt L1 + dt^2/6 (Lt1 + 2 Lt2) (integrator.hpp:72-74)
-                    //         = A + dt^2/6 * 2 Lt2, A formed by stage 1
-#pragma unroll
-                    for (int m = 0; m < N; ++m) {
-                        const double L = R[m] * (ctab<P, DIM>.massf[m] * ivol);
-                        if (valid) out0[g0 + (long)(m * 5) * kp.cs] = ab[(m * 5 + v) * TC + l] + c6 * (2.0 * L);
+                for (int m = 0; m < N; ++m) {
+                    const double L = R[m] * (ctab<P, DIM>.massf[m] * ivol);
+                    const long gi = g0 + (long)(m * 5) * kp.cs;
+                    if (MODE == MODE_STAGE1) {
+                        lb[(ft * NC + m * 5 + v) * TC + l] = L;
+                    } else {
+                        // q^{n+1} = q + dt L1 + dt^2/6 (Lt1 + 2 Lt2) (integrator.hpp:72-74)
+                        // = A + dt^2/6 * 2 Lt2, A formed by stage 1
+                        out0[gi] = ab[(m * 5 + v) * TC + l] + c6 * (2.0 * L);
                     }
                 }
             }
         }
+        if (MODE == MODE_STAGE1) {
+            // from shared memory, per coefficient (integrator.hpp:69-74):
+            //   q* = q + dt/2 L1 + dt^2/8 Lt1           -> out0
+            //   A  = q + (dt L1 + dt^2/6 Lt1)           -> out1 (stage 2 adds dt^2/6 * 2 Lt2)
+            race_shake(kp, 4, n);
+            __syncthreads();
+            const double c6 = dt * dt / 6.0;
+            // unrolled with predicated stores: all shared-memory loads of the
+            // thread's elements issue before the first use
+#pragma unroll
+            for (int e = tid; e < NC * TC; e += NT) {
+                const int l = e % TC, comp = e / TC;
+                const double q = sc[comp * TC + l], L = lb[comp * TC + l], Lt = lb[(NC + comp) * TC + l];
+                const long gi = comp * kp.cs + cbase + i0 + l;
+                if (i0 + l < nx) {
+                    out0[gi] = q + 0.5 * dt * L + 0.125 * dt * dt * Lt;
+                    out1[gi] = q + (dt * L + c6 * Lt);
+                }
+            }
+        }
+#if HGKS_CELL_ENDBAR
+        race_shake(kp, 5, n);
+        __syncthreads();  // buffers of this tile are free for the next prefetch
+#endif
         cur = nxt;
     }
     cp_async_wait<0>();

@@ -9,22 +9,25 @@
 namespace hgks_dev {
 
 struct KernelSet {
-    void (*face)(const KParams&, const double* q, double* const f[3], cudaStream_t, int report,
-                 const int* tile);
+    // qmap: the two TMA tensor maps of q (x, row, comp) — box {32, 1, NC} for
+    // the y / z faces, {34, 1, NC} for the x faces — or null (cp.async staging)
+    void (*face)(const KParams&, const double* q, const CUtensorMap* qmap, double* const f[3], cudaStream_t,
+                 int report, const int* tile);
     void (*cell)(const KParams&, int mode, const double* qin, double* const f[3], const double* qn,
                  const double* L1, const double* Lt1, double* o0, double* o1, double* o2,
                  cudaStream_t, int report, const int* tile);
     // the same kernels restricted to owned z layers [kb, ke) (all three face
     // axes / the cell update of those layers), for the streamed host step
-    void (*face_layers)(const KParams&, const double* q, double* const f[3], cudaStream_t, int kb,
-                        int ke);
+    void (*face_layers)(const KParams&, const double* q, const CUtensorMap* qmap, double* const f[3],
+                        cudaStream_t, int kb, int ke);
     // one face axis over z layers [kb, ke) (z: up to zface_layers), for the
     // multi-slab step that overlaps the halo exchange with interior faces
-    void (*face_axis)(const KParams&, int axis, const double* q, double* f, cudaStream_t, int kb,
-                      int ke);
+    void (*face_axis)(const KParams&, int axis, const double* q, const CUtensorMap* qmap, double* f,
+                      cudaStream_t, int kb, int ke);
     void (*cell_layers)(const KParams&, int mode, const double* qin, double* const f[3],
                         const double* qn, const double* L1, const double* Lt1, double* o0,
                         double* o1, double* o2, cudaStream_t, int kb, int ke);
+    int face_tma;  // 1: the face kernels can stage by TMA (given qmap)
     int face_smem[3];
     int cell_smem;
     int cell_tc;

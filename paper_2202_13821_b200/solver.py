@@ -366,6 +366,12 @@ class Solver:
         self.L.hgks_kernel_times(self.h, ctypes.byref(f), ctypes.byref(c), ctypes.byref(o))
         return f.value, c.value
 
+    def kernel_times_stage(self, stage: int):
+        """(face ms, cell ms) of one S2O4 stage of the last timed step."""
+        f, c = ctypes.c_double(), ctypes.c_double()
+        self._check(self.L.hgks_kernel_times_stage(self.h, stage, ctypes.byref(f), ctypes.byref(c)))
+        return f.value, c.value
+
     # -- multi-slab plumbing (SURVEY §8e)
     def halo_bytes(self) -> int:
         return self.L.hgks_halo_bytes(self.h)
@@ -461,6 +467,10 @@ class Solver:
     def set_grid_cap(self, ctas: int):
         """Test hook: cap the persistent grids (every CTA walks many tiles)."""
         self.L.hgks_set_grid_cap(self.h, int(ctas))
+
+    def set_face_tma(self, on: bool = True):
+        """Face-kernel staging: TMA boxes (default, even nx) or per-lane cp.async."""
+        self.L.hgks_set_face_tma(self.h, int(on))
 
     def set_race_shake(self, seed: int):
         """Test hook: randomized per-warp delays before every cp.async wait and

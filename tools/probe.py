@@ -11,6 +11,8 @@ t0 = time.time()
 r = P.setup_run(P.CaseConfig.named(case, n), P.RunOptions(degree=deg))
 print("setup", time.time() - t0)
 s = r.solver
+import os
+s.set_face_tma(os.environ.get("HGKS_FACE_TMA", "1") != "0")
 s.set_kernel_timing(True)
 dt = s.compute_dt(0.15)
 print("dt", dt)
