@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of CPU reference work")
     ap.add_argument("--face-staging", default="tma", choices=["tma", "cpasync"],
                     help="face-kernel staging: TMA boxes (default) or per-lane cp.async (A/B)")
+    ap.add_argument("--cell-staging", default="tma", choices=["tma", "cpasync"],
+                    help="cell-kernel staging: TMA boxes (default) or per-lane cp.async (A/B)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo = host-staged halo exchange (multi-rank test mode on one GPU)")
     return ap.parse_args()
@@ -234,6 +236,7 @@ def main():
     torch.cuda.set_stream(stream)
     s.set_stream(stream.cuda_stream)
     s.set_face_tma(a.face_staging == "tma")
+    s.set_cell_tma(a.cell_staging == "tma")
     if world > 1:
         # nccl: the library's own data plane (halo send/recv, dt and error-key
         # reductions inside the per-step graph); gloo: the host-staged test mode
@@ -447,7 +450,7 @@ def main():
         "config": {"workload": workload(a), "case": a.case, "n": a.n, "degree": a.degree,
                    "cells": ncell_glob, "dof": dof_glob, "parallelism": f"z-slab x{world}",
                    "halo_transport": a.dist_backend if world > 1 else None,
-                   "face_staging": a.face_staging,
+                   "face_staging": a.face_staging, "cell_staging": a.cell_staging,
                    "l2": "inputs larger than L2 (state 839 MB at 128^3 P2); no flush"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -244,6 +244,9 @@ void hgks_set_race_shake(hgks_solver* s, unsigned seed);
 /* face-kernel staging: 1 (default) = TMA boxes (cp.async.bulk.tensor +
  * mbarrier) when nx is even, 0 = per-lane cp.async (A/B and tests) */
 void hgks_set_face_tma(hgks_solver* s, int on);
+/* cell-kernel staging of the coefficient, face-flux and stage-2 A tiles: 1
+ * (default) = TMA boxes when nx is even, 0 = per-lane cp.async */
+void hgks_set_cell_tma(hgks_solver* s, int on);
 
 /* Roofline denominator: sustained FP64 FMA throughput of `device`, measured
  * with a DFMA-chain kernel over ~`ms` milliseconds (CUDA events). Writes

@@ -32,7 +32,7 @@ EXPORTS = [
     "hgks_halo_pack", "hgks_halo_unpack", "hgks_set_halo_exchange", "hgks_set_halo_exchange_split", "hgks_step_phase",
     "hgks_set_host_reduce", "hgks_nccl_unique_id", "hgks_attach_nccl", "hgks_attach_nccl_comm",
     "hgks_slab_reduce_sum", "hgks_set_stream", "hgks_get_stream", "hgks_synchronize",
-    "hgks_launch_count", "hgks_set_kernel_timing", "hgks_kernel_times", "hgks_kernel_times_stage", "hgks_set_graphs", "hgks_set_grid_cap", "hgks_set_race_shake", "hgks_set_face_tma",
+    "hgks_launch_count", "hgks_set_kernel_timing", "hgks_kernel_times", "hgks_kernel_times_stage", "hgks_set_graphs", "hgks_set_grid_cap", "hgks_set_race_shake", "hgks_set_face_tma", "hgks_set_cell_tma",
     "hgks_measure_fp64_peak",
 ]
 
@@ -126,6 +126,8 @@ def load():
     L.hgks_set_race_shake.restype = None
     L.hgks_set_face_tma.argtypes = [sp, ctypes.c_int]
     L.hgks_set_face_tma.restype = None
+    L.hgks_set_cell_tma.argtypes = [sp, ctypes.c_int]
+    L.hgks_set_cell_tma.restype = None
     L.hgks_set_stream.argtypes = [sp, sp]
     L.hgks_get_stream.argtypes = [sp]
     L.hgks_get_stream.restype = sp

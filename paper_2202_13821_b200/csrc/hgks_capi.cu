@@ -67,6 +67,11 @@ struct hgks_solver {
     CUtensorMap qmap[3][2];
     bool have_qmap = false;  // maps built (even nx)
     bool face_tma = true;    // use them (hgks_set_face_tma)
+    // cell kernel: state / A maps with box {TC, 1, NC} ([buf0, buf1, qs, A]),
+    // face maps [axis][RW 10 | RW 5] with box {XS | TC, 1, RW, nfp}
+    CUtensorMap cstate[4], cface[3][2];
+    bool have_cmap = false;
+    bool cell_tma = true;
     unsigned long long* d_key = nullptr;  // K_* words (hgks_aux_kernels.cuh)
     double* d_val = nullptr;              // report value of a failure
     double* d_red = nullptr;              // reduction scratch
@@ -196,7 +201,48 @@ int make_qmaps(hgks_solver* s) {
                 return fail(s, HGKS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
         }
     s->have_qmap = true;
+    // cell kernel maps
+    const int TC = s->ks.cell_tc, XS = s->ks.cell_xs;
+    double* sarr[4] = {s->buf[0], s->buf[1], s->qs, s->A};
+    for (int a = 0; a < 4; ++a) {
+        const cuuint64_t dims[3] = {(cuuint64_t)s->nx, (cuuint64_t)s->ny * (s->nzl + 2), (cuuint64_t)s->NC};
+        const cuuint64_t strides[2] = {(cuuint64_t)s->nx * 8, (cuuint64_t)s->cs * 8};
+        const cuuint32_t box[3] = {(cuuint32_t)TC, 1, (cuuint32_t)s->NC};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        if (encode(&s->cstate[a], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, sarr[a], dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return fail(s, HGKS_ERR_CUDA, "cuTensorMapEncodeTiled failed (cell state map)");
+    }
+    for (int ax = 0; ax < 3; ++ax)
+        for (int v = 0; v < 2; ++v) {
+            const int RW = v == 0 ? 10 : 5, nfp = s->ks.nfp[ax];
+            const cuuint64_t dims[4] = {(cuuint64_t)s->nx, (cuuint64_t)s->ny * (s->nzl + 1), 10, (cuuint64_t)nfp};
+            const cuuint64_t strides[3] = {(cuuint64_t)s->nx * 8, (cuuint64_t)s->fs * 8, (cuuint64_t)s->fs * 80};
+            const cuuint32_t box[4] = {(cuuint32_t)(ax == 0 ? XS : TC), 1, (cuuint32_t)RW, (cuuint32_t)nfp};
+            const cuuint32_t estr[4] = {1, 1, 1, 1};
+            if (encode(&s->cface[ax][v], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s->face[ax], dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return fail(s, HGKS_ERR_CUDA, "cuTensorMapEncodeTiled failed (cell face map)");
+        }
+    s->have_cmap = true;
     return HGKS_OK;
+}
+
+// the cell launch's maps: the input state, A, and the mode's face boxes
+// (null: cp.async staging)
+const CellMaps* cmaps_for(hgks_solver* s, const double* qin, int mode, CellMaps& cm) {
+    if (!s->have_cmap || !s->cell_tma) return nullptr;
+    const int a = qin == s->buf[0] ? 0 : qin == s->buf[1] ? 1 : qin == s->qs ? 2 : -1;
+    if (a < 0) return nullptr;
+    const int v = mode == MODE_STAGE2 ? 1 : 0;
+    cm.coef = s->cstate[a];
+    cm.A = s->cstate[3];
+    cm.fx = s->cface[0][v];
+    cm.fy = s->cface[1][v];
+    cm.fz = s->cface[2][v];
+    return &cm;
 }
 
 KParams make_params(hgks_solver* s, int stage, int slot) {
@@ -220,6 +266,7 @@ KParams make_params(hgks_solver* s, int stage, int slot) {
     kp.grid_cap = s->grid_cap;
     kp.shake = s->shake;
     kp.face_tma = s->have_qmap && s->face_tma ? 1 : 0;
+    kp.cell_tma = s->have_cmap && s->cell_tma ? 1 : 0;
     kp.gas.gamma = s->cfg.gamma;
     kp.gas.gm1 = s->cfg.gamma - 1.0;
     kp.gas.K = (5.0 - 3.0 * s->cfg.gamma) / (s->cfg.gamma - 1.0);
@@ -402,7 +449,10 @@ int run_residual(hgks_solver* s, double* in, int stage, int slot, int mode, doub
         s->launches += 3;
     }
     ev_record(s, stage * 3 + 1);
-    s->ks.cell(kp, mode, in, s->face, nullptr, s->A, nullptr, o0, o1, nullptr, s->stream, 0, nullptr);
+    CellMaps cm;
+    const CellMaps* cmp = cmaps_for(s, in, mode, cm);
+    if (!cmp) kp.cell_tma = 0;
+    s->ks.cell(kp, cmp, mode, in, s->face, nullptr, s->A, nullptr, o0, o1, nullptr, s->stream, 0, nullptr);
     s->launches += 1;
     ev_record(s, stage * 3 + 2);
     CK(cudaGetLastError());
@@ -473,7 +523,10 @@ int finish_error(hgks_solver* s, unsigned long long key, double* const stage_inp
             tile[1] = j;
             tile[2] = k;
             tile[3] = 0;
-            s->ks.cell(kp, MODE_RESIDUAL, in, s->face, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+            CellMaps cm;
+            const CellMaps* cmp = cmaps_for(s, in, MODE_RESIDUAL, cm);
+            if (!cmp) kp.cell_tma = 0;
+            s->ks.cell(kp, cmp, MODE_RESIDUAL, in, s->face, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                        s->stream, 1, tile);
         }
     }, &val);
@@ -1161,13 +1214,21 @@ int hgks_two_stage_step_host_streamed(hgks_solver* s, double* q, double dt, int 
     };
     auto F1 = [&](int c) { K.face_layers(kp1, qn, qmap_of(s, qn), s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
     auto C1 = [&](int c) {
-        K.cell_layers(kp1, MODE_STAGE1, qn, s->face, nullptr, nullptr, nullptr, s->qs, s->A, nullptr, cs,
+        CellMaps cm;
+        const CellMaps* cmp = cmaps_for(s, qn, MODE_STAGE1, cm);
+        KParams k1 = kp1;
+        if (!cmp) k1.cell_tma = 0;
+        K.cell_layers(k1, cmp, MODE_STAGE1, qn, s->face, nullptr, nullptr, nullptr, s->qs, s->A, nullptr, cs,
                       kb(c), kb(c + 1));
         ++s->launches;
     };
     auto F2 = [&](int c) { K.face_layers(kp2, s->qs, qmap_of(s, s->qs), s->face, cs, kb(c), kb(c + 1)); s->launches += 3; };
     auto C2 = [&](int c) {
-        K.cell_layers(kp2, MODE_STAGE2, s->qs, s->face, nullptr, s->A, nullptr, qnew, nullptr, nullptr, cs,
+        CellMaps cm;
+        const CellMaps* cmp = cmaps_for(s, s->qs, MODE_STAGE2, cm);
+        KParams k2 = kp2;
+        if (!cmp) k2.cell_tma = 0;
+        K.cell_layers(k2, cmp, MODE_STAGE2, s->qs, s->face, nullptr, s->A, nullptr, qnew, nullptr, nullptr, cs,
                       kb(c), kb(c + 1));
         // q^{n+1} of chunk c -> AoS staging for its download
         soa_to_aos_kernel<<<tblocks, 256, 0, cs>>>(kp0, qnew, s->tmp2, NC, kb(c) * S, kb(c + 1) * S);
@@ -1581,6 +1642,11 @@ void hgks_set_grid_cap(hgks_solver* s, int ctas) {
 void hgks_set_face_tma(hgks_solver* s, int on) {
     drop_graphs(s);
     s->face_tma = on != 0;
+}
+
+void hgks_set_cell_tma(hgks_solver* s, int on) {
+    drop_graphs(s);
+    s->cell_tma = on != 0;
 }
 
 void hgks_set_race_shake(hgks_solver* s, unsigned seed) {

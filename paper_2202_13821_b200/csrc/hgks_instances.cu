@@ -19,6 +19,11 @@ inline const CUtensorMap& map_or_null(const CUtensorMap* m) {
     return m ? *m : zero;
 }
 
+inline const CellMaps& cmaps_or_null(const CellMaps* m) {
+    static const CellMaps zero{};
+    return m ? *m : zero;
+}
+
 // persistent grid size: resident CTAs on the GPU, optionally capped
 // (KParams::grid_cap, a test hook that makes every CTA walk many tiles)
 inline int capped(const KParams& kp, int g) {
@@ -90,7 +95,7 @@ struct Launch {
         face_axis_layers<1>(kp, q, qm, f[1], st, kb, ke);
         face_axis_layers<2>(kp, q, qm, f[2], st, kb, ke);
     }
-    static void cell_layers(const KParams& kp, int mode, const double* qin, double* const f[3],
+    static void cell_layers(const KParams& kp, const CellMaps* cm, int mode, const double* qin, double* const f[3],
                             const double* qn, const double* L1, const double* Lt1, double* o0,
                             double* o1, double* o2, cudaStream_t st, int kb, int ke) {
         const int ntx = (kp.nx + SH::TC - 1) / SH::TC;
@@ -100,11 +105,11 @@ struct Launch {
         if (mode == MODE_STAGE1)
             cell_kernel<P, DIM, VISC, MODE_STAGE1><<<grid, CellTile<P, DIM, MODE_STAGE1>::NT,
                                                      cell_smem<MODE_STAGE1>(), st>>>(
-                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, cmaps_or_null(cm));
         else
             cell_kernel<P, DIM, VISC, MODE_STAGE2><<<grid, CellTile<P, DIM, MODE_STAGE2>::NT,
                                                      cell_smem<MODE_STAGE2>(), st>>>(
-                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, cmaps_or_null(cm));
     }
     static void face(const KParams& kp, const double* q, const CUtensorMap* qm, double* const f[3], cudaStream_t st,
                      int report, const int* tile) {
@@ -113,7 +118,7 @@ struct Launch {
         if (!report || tile[3] == 1) face_axis<1>(kp, q, qm, f[1], st, report, tile);
         if (!report || tile[3] == 2) face_axis<2>(kp, q, qm, f[2], st, report, tile);
     }
-    static void cell(const KParams& kp, int mode, const double* qin, double* const f[3],
+    static void cell(const KParams& kp, const CellMaps* cm, int mode, const double* qin, double* const f[3],
                      const double* qn, const double* L1, const double* Lt1, double* o0, double* o1,
                      double* o2, cudaStream_t st, int report, const int* tile) {
         const int ntx = (kp.nx + SH::TC - 1) / SH::TC;
@@ -128,15 +133,15 @@ struct Launch {
         if (mode == MODE_RESIDUAL)
             cell_kernel<P, DIM, VISC, MODE_RESIDUAL><<<grid, CellTile<P, DIM, MODE_RESIDUAL>::NT,
                                                        cell_smem<MODE_RESIDUAL>(), st>>>(
-                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, cmaps_or_null(cm));
         else if (mode == MODE_STAGE1)
             cell_kernel<P, DIM, VISC, MODE_STAGE1><<<grid, CellTile<P, DIM, MODE_STAGE1>::NT,
                                                      cell_smem<MODE_STAGE1>(), st>>>(
-                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, cmaps_or_null(cm));
         else
             cell_kernel<P, DIM, VISC, MODE_STAGE2><<<grid, CellTile<P, DIM, MODE_STAGE2>::NT,
                                                      cell_smem<MODE_STAGE2>(), st>>>(
-                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, 0);
+                kp, qin, f[0], f[1], f[2], qn, L1, Lt1, o0, o1, o2, first, count, cmaps_or_null(cm));
     }
     static cudaError_t configure() {
         cudaError_t e = cudaSuccess;
@@ -190,6 +195,7 @@ struct Launch {
         k.cell_smem = cell_smem();
         k.cell_tc = SH::TC;
         k.face_tma = HGKS_FACE_STAGES == 2;  // the TMA path needs the double-buffered stage
+        k.cell_xs = CellTile<P, DIM, MODE_STAGE1>::XS;
         k.nfp[0] = SH::template nfp<0>();
         k.nfp[1] = SH::template nfp<1>();
         k.nfp[2] = SH::template nfp<2>();

@@ -52,11 +52,6 @@
 #ifndef HGKS_CELL_NT3
 #define HGKS_CELL_NT3 160
 #endif
-// cell kernel: end-of-tile barrier before the next tile's face prefetch (1)
-// or face / coefficient prefetch issued after the top barrier (0)
-#ifndef HGKS_CELL_ENDBAR
-#define HGKS_CELL_ENDBAR 0
-#endif
 // cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
 #ifndef HGKS_CELL_TC
 #define HGKS_CELL_TC 16
@@ -114,6 +109,7 @@ struct KParams {
     int grid_cap;          // > 0: cap on the persistent grids (tests: many tiles per CTA)
     unsigned shake;        // != 0: race shaker seed (tests; see race_shake)
     int face_tma;          // 1: face kernels stage by TMA (the qmap argument is valid)
+    int cell_tma;          // 1: cell kernels stage by TMA (the CellMaps argument is valid)
     GasC gas;
     const double* dx;      // [nx] widths
     const double* dy;      // [ny]
@@ -401,6 +397,15 @@ struct FaceStage {
     static constexpr int RSL = AXIS == 0 ? 34 : 32, RSR = RSL;
     static constexpr int OFL = AXIS == 0 ? 1 : 0, OFR = AXIS == 0 ? 2 : NC * 32;
 };
+
+__device__ __forceinline__ void tma_load4(double* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                          uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(
+            (unsigned)__cvta_generic_to_shared(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"((unsigned)__cvta_generic_to_shared(bar))
+        : "memory");
+}
 
 // Persistent face kernel. A CTA = NFP warps; each tile is 32 consecutive faces
 // along x (one lane each) at one (j, k), one face point per warp, so the
@@ -758,7 +763,9 @@ enum : int { MODE_RESIDUAL = 0, MODE_STAGE1 = 1, MODE_STAGE2 = 2 };
 
 // shared-memory plan of one cell-kernel CTA (doubles). Face and volume flux
 // rows are (F|Ft) x var; the S2O4 second stage keeps only the Ft rows
-// (RW = 5, RO = 5), so its tile is half as large.
+// (RW = 5, RO = 5), so its tile is half as large. Every region starts
+// 128-byte aligned (TMA destinations): sizes rounded to 16 doubles.
+constexpr int pad16(int n) { return (n + 15) / 16 * 16; }
 template <int P, int DIM, int MODE>
 struct CellTile {
     using SH = Shape<P, DIM>;
@@ -766,17 +773,23 @@ struct CellTile {
     static constexpr int NFX = SH::template nfp<0>(), NFY = SH::template nfp<1>(),
                          NFZ = SH::template nfp<2>();
     static constexpr int RW = MODE == MODE_STAGE2 ? 5 : 10, RO = 10 - RW;
-    static constexpr int COEF = NC * TC;           // one coefficient tile [NC][TC]
-    static constexpr int FX = NFX * RW * (TC + 1); // x faces i0..i0+TC   [pf*RW+c][TC+1]
-    static constexpr int FY = NFY * RW * 2 * TC;   // y faces rows j, j+1 [pf*RW+c][2][TC]
-    static constexpr int FZ = NFZ * RW * 2 * TC;   // z faces layers k, k+1
-    static constexpr int VFW = 3 * RW;             // flux rows per volume point
-    static constexpr int VF = NVP * VFW * TC;      // volume-point fluxes [p][VFW][TC]
-    static constexpr int LB = MODE == MODE_STAGE1 ? 2 * NC * TC : 0;  // L, Lt of the tile (stage-1 q*)
-    static constexpr int GEO = 2 * TC + 4;          // widths of a tile: dx, 2/dx [TC]; dy, dz, 2/dy, 2/dz
+    static constexpr int XS = TC + 2;                    // x faces i0..i0+TC (+1 pad: even box width)
+    static constexpr int COEF = pad16(NC * TC);          // one coefficient tile [NC][TC]
+    static constexpr int FX = pad16(NFX * RW * XS);      // x faces [pf][c][XS]
+    static constexpr int FYH = pad16(NFY * RW * TC);     // y faces of one row [pf][c][TC]
+    static constexpr int FZH = pad16(NFZ * RW * TC);
+    static constexpr int FY = pad16(2 * FYH);            // rows j, j+1   [half][pf][c][TC]
+    static constexpr int FZ = pad16(2 * FZH);            // layers k, k+1 [half][pf][c][TC]
+    static constexpr int VFW = 3 * RW;                   // flux rows per volume point
+    static constexpr int VF = pad16(NVP * VFW * TC);     // volume-point fluxes [p][VFW][TC]
+    static constexpr int LB = MODE == MODE_STAGE1 ? pad16(2 * NC * TC) : 0;  // L, Lt of the tile (stage-1 q*)
+    static constexpr int GEO = 2 * TC + 4;               // widths of a tile: dx, 2/dx [TC]; dy, dz, 2/dy, 2/dz
     // stage 2: the tile's A = q + dt L1 + dt^2/6 Lt1 [NC][TC], prefetched with the faces
     static constexpr int AB = MODE == MODE_STAGE2 ? COEF : 0;
-    static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + LB + 2 * GEO + AB;
+    static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + LB + AB + pad16(2 * GEO);
+    // bytes the face group of a tile lands (TMA transaction count)
+    static constexpr unsigned FACE_TX =
+        8u * (NFX * RW * XS + 2 * NFY * RW * TC + 2 * NFZ * RW * TC + (MODE == MODE_STAGE2 ? NC * TC : 0));
     // threads / resident CTAs: stage 2 (half the tile, ~150 registers) runs
     // one thread per (cell, volume point) at 3 CTAs per SM for 3-D P1/P2
     static constexpr bool S2X = MODE == MODE_STAGE2 && P < 3 && DIM == 3;
@@ -784,9 +797,17 @@ struct CellTile {
     static constexpr int MINB = S2X ? 3 : SH::MINB_CELL;
 };
 
+// TMA tensor maps of one cell-kernel launch: the input state and stage 2's A
+// (box {TC, 1, NC} of the (x, row, comp) view), the three face buffers (box
+// {XS | TC, 1, RW, nfp} of the (x, row, F|Ft x var, point) view)
+struct CellMaps {
+    CUtensorMap coef, A, fx, fy, fz;
+};
+
 // Persistent CTA over tiles of TC consecutive cells along x, software
 // pipelined: while tile t is computed, the coefficients of tile t+grid and
-// the face fluxes of tile t stream into shared memory (cp.async).
+// the face fluxes of tile t stream into shared memory — by TMA
+// (KParams::cell_tma: one elected thread, mbarrier completion) or cp.async.
 // Phase B: one (cell, volume point) item per thread -> smooth fluxes.
 // Phase C: one (cell, var, F|Ft) item per thread -> face gather + volume
 // projection + M^-1 (+ S2O4 combine); stage 1 then forms q* per coefficient
@@ -798,21 +819,25 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
                 const double* __restrict__ qn, const double* __restrict__ L1,
                 const double* __restrict__ Lt1, double* __restrict__ out0,
                 double* __restrict__ out1, double* __restrict__ out2, int tile_first,
-                int tile_count, int unused) {
+                int tile_count, const __grid_constant__ CellMaps maps) {
     using SH = Shape<P, DIM>;
     using CT = CellTile<P, DIM, MODE>;
-    constexpr int N = SH::N, NC = SH::NC, NVP = SH::NVP, TC = SH::TC;
+    constexpr int N = SH::N, NC = SH::NC, NVP = SH::NVP, TC = SH::TC, XS = CT::XS;
     constexpr int NT = CT::NT, NAX = SH::NAX;
     extern __shared__ __align__(128) double smem[];  // 128 B: TMA destinations
     double* coefb = smem;                 // [2][NC][TC]
-    double* fx = coefb + 2 * CT::COEF;
-    double* fy = fx + CT::FX;
+    double* fx = coefb + 2 * CT::COEF;    // [pf][c][XS]
+    double* fy = fx + CT::FX;             // [half][pf][c][TC]
     double* fz = fy + CT::FY;
     double* vf = fz + CT::FZ;             // [NVP][VFW][TC]
     double* lb = vf + CT::VF;             // [2][NC][TC]
-    double* geob = lb + CT::LB;           // [2][GEO], staged with the coefficients
-    double* ab = geob + 2 * CT::GEO;      // [NC][TC] stage 2: A of the tile
+    double* ab = lb + CT::LB;             // [NC][TC] stage 2: A of the tile
+    double* geob = ab + CT::AB;           // [2][GEO], staged with the coefficients
+    __shared__ uint64_t mb_c[2], mb_f;    // TMA: coefficient buffers, face group
 
+    if (kp.scal[SC_ACTIVE] == 0.0) return;  // halted device loop: no-op step
+    const double dt = kp.scal[SC_DT];
+    const bool tma = kp.cell_tma != 0;
     const int tid = threadIdx.x;
     const int nx = kp.nx, ny = kp.ny;
     const int ntx = (nx + TC - 1) / TC;
@@ -834,16 +859,15 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
 #pragma unroll 4
             for (int comp = tid / TC; comp < NC; comp += CST, src += sst) cp_async8(dst + comp * TC + l, src, ok);
         } else {
-            for (int e = tid; e < CT::COEF; e += NT) {
+            for (int e = tid; e < NC * TC; e += NT) {
                 const int l = e % TC, comp = e / TC;
                 const bool ok = ti.i0 + l < nx;
                 cp_async8(dst + comp * TC + l, base + comp * kp.cs + cbase + (ok ? ti.i0 + l : 0), ok);
             }
         }
     };
-    auto prefetch_coef = [&](const TI& ti, double* dst, double* gdst) {
-        // the tile's widths ride along (loaded through the async copy so their
-        // latency is hidden like the coefficients')
+    // the tile's widths (always cp.async, by TC + 4 threads)
+    auto prefetch_geo = [&](const TI& ti, double* gdst) {
         if (tid < TC) {
             const bool ok = ti.i0 + tid < nx;
             const int i = ok ? ti.i0 + tid : 0;
@@ -855,19 +879,39 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
                                                                                           : kp.i2dz + ti.k + 1;
             cp_async8(gdst + 2 * TC + r, src, true);
         }
-        prefetch_state(qin, ti, dst);
+    };
+    auto coef_tma = [&](const TI& ti, double* dst, uint64_t* bar) {
+        mbar_expect_tx(bar, 8u * NC * TC);
+        tma_load3(dst, &maps.coef, ti.i0, ti.j + ny * (ti.k + 1), 0, bar);
     };
     // stage 2 consumes only the Ft rows (the face pass stores only those)
     constexpr int RW = CT::RW, RO = CT::RO;
-    auto face_row = [](int rr) { return (rr / RW) * 10 + RO + rr % RW; };
+    auto face_rows = [&](const TI& ti, long& rowk, long& rowp, long& rowz, int& jp, int& kp1) {
+        rowk = (long)nx * (ti.j + (long)ny * ti.k);
+        jp = ti.j + 1 == ny ? 0 : ti.j + 1;
+        rowp = (long)nx * (jp + (long)ny * ti.k);
+        kp1 = (ti.k + 1 == kp.zface_layers && kp.z_wrap) ? 0 : ti.k + 1;
+        rowz = (long)nx * (ti.j + (long)ny * kp1);
+    };
+    auto faces_tma = [&](const TI& ti) {
+        long rowk, rowp, rowz;
+        int jp, kp1;
+        face_rows(ti, rowk, rowp, rowz, jp, kp1);
+        mbar_expect_tx(&mb_f, CT::FACE_TX);
+        const int r0 = ti.j + ny * ti.k;
+        tma_load4(fx, &maps.fx, ti.i0, r0, RO, 0, &mb_f);
+        tma_load4(fy, &maps.fy, ti.i0, r0, RO, 0, &mb_f);
+        tma_load4(fy + CT::FYH, &maps.fy, ti.i0, jp + ny * ti.k, RO, 0, &mb_f);
+        tma_load4(fz, &maps.fz, ti.i0, r0, RO, 0, &mb_f);
+        tma_load4(fz + CT::FZH, &maps.fz, ti.i0, ti.j + ny * kp1, RO, 0, &mb_f);
+        if (MODE == MODE_STAGE2) tma_load3(ab, &maps.A, ti.i0, ti.j + ny * (ti.k + 1), 0, &mb_f);
+    };
     auto prefetch_faces = [&](const TI& ti) {
         if (MODE == MODE_STAGE2) prefetch_state(L1, ti, ab);
-        const int i0 = ti.i0, j = ti.j, k = ti.k;
-        const long rowk = (long)nx * (j + (long)ny * k);
-        const int jp = j + 1 == ny ? 0 : j + 1;
-        const long rowp = (long)nx * (jp + (long)ny * k);
-        const int kp1 = (k + 1 == kp.zface_layers && kp.z_wrap) ? 0 : k + 1;
-        const long rowz = (long)nx * (j + (long)ny * kp1);
+        const int i0 = ti.i0;
+        long rowk, rowp, rowz;
+        int jp, kp1;
+        face_rows(ti, rowk, rowp, rowz, jp, kp1);
         if constexpr (2 * TC == 32) {
             // one face row per warp instruction: x rows hold TC+1 faces
             // (lanes 0..TC), y/z rows the TC faces of both neighbour rows
@@ -878,8 +922,9 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
             const long ox = rowk + (okx ? (igx == nx ? 0 : igx) : 0);
             const int ig = i0 + (lane % TC);
             const bool ok = ig < nx;
-            const long oy = (lane < TC ? rowk : rowp) + (ok ? ig : 0);
-            const long oz = (lane < TC ? rowk : rowz) + (ok ? ig : 0);
+            const int half = lane < TC ? 0 : 1;
+            const long oy = (half ? rowp : rowk) + (ok ? ig : 0);
+            const long oz = (half ? rowz : rowk) + (ok ? ig : 0);
             // a warp owns component rows c (F/Ft x var) and walks the face
             // points with constant strides: row pf*10 + RO + c
             const long pst = 10 * kp.fs;
@@ -890,72 +935,84 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
                 const double* sz = f2 + (long)r0 * kp.fs + oz;
 #pragma unroll
                 for (int pf = 0; pf < CT::NFX; ++pf)
-                    if (lane <= TC) cp_async8(fx + (pf * RW + c) * (TC + 1) + lane, sx + pf * pst, okx);
+                    if (lane <= TC) cp_async8(fx + (pf * RW + c) * XS + lane, sx + pf * pst, okx);
 #pragma unroll
                 for (int pf = 0; pf < CT::NFY; ++pf)
-                    cp_async8(fy + (pf * RW + c) * 2 * TC + lane, sy + pf * pst, ok);
+                    cp_async8(fy + half * CT::FYH + (pf * RW + c) * TC + lane % TC, sy + pf * pst, ok);
 #pragma unroll
                 for (int pf = 0; pf < CT::NFZ; ++pf)
-                    cp_async8(fz + (pf * RW + c) * 2 * TC + lane, sz + pf * pst, ok);
+                    cp_async8(fz + half * CT::FZH + (pf * RW + c) * TC + lane % TC, sz + pf * pst, ok);
             }
         } else {
+            auto row_of = [](int rr) { return (rr / RW) * 10 + RO + rr % RW; };
             for (int e = tid; e < CT::NFX * RW * (TC + 1); e += NT) {  // x faces i0 .. i0+TC (periodic wrap at nx)
-                const int l = e % (TC + 1), r = face_row(e / (TC + 1));
+                const int l = e % (TC + 1), rr = e / (TC + 1);
                 const int ig = i0 + l;
                 const bool ok = ig <= nx;  // x is always periodic: face nx is face 0
                 const int iw = ig == nx ? 0 : ig;
-                cp_async8(fx + e, f0 + (long)r * kp.fs + rowk + (ok ? iw : 0), ok);
+                cp_async8(fx + rr * XS + l, f0 + (long)row_of(rr) * kp.fs + rowk + (ok ? iw : 0), ok);
             }
             for (int e = tid; e < CT::NFY * RW * 2 * TC; e += NT) {  // y faces of rows j, j+1
-                const int l = e % (2 * TC), r = face_row(e / (2 * TC));
-                const int ig = i0 + (l % TC);
+                const int l = e % TC, rr = (e / TC) % (CT::NFY * RW), half = e / (TC * CT::NFY * RW);
+                const int ig = i0 + l;
                 const bool ok = ig < nx;
-                cp_async8(fy + e, f1 + (long)r * kp.fs + (l < TC ? rowk : rowp) + (ok ? ig : 0), ok);
+                cp_async8(fy + half * CT::FYH + rr * TC + l,
+                          f1 + (long)row_of(rr) * kp.fs + (half ? rowp : rowk) + (ok ? ig : 0), ok);
             }
             for (int e = tid; e < CT::NFZ * RW * 2 * TC; e += NT) {  // z faces of layers k, k+1
-                const int l = e % (2 * TC), r = face_row(e / (2 * TC));
-                const int ig = i0 + (l % TC);
+                const int l = e % TC, rr = (e / TC) % (CT::NFZ * RW), half = e / (TC * CT::NFZ * RW);
+                const int ig = i0 + l;
                 const bool ok = ig < nx;
-                cp_async8(fz + e, f2 + (long)r * kp.fs + (l < TC ? rowk : rowz) + (ok ? ig : 0), ok);
+                cp_async8(fz + half * CT::FZH + rr * TC + l,
+                          f2 + (long)row_of(rr) * kp.fs + (half ? rowz : rowk) + (ok ? ig : 0), ok);
             }
         }
     };
-    if (kp.scal[SC_ACTIVE] == 0.0) return;  // halted device loop: no-op step
-    const double dt = kp.scal[SC_DT];
     const int t0 = tile_first + (kp.report ? 0 : blockIdx.x);
     TI cur = walk.of(t0);
-    if (t0 < tile_end) prefetch_coef(cur, coefb, geob);
+    if (tma) {
+        if (tid == 0) {
+            mbar_init(&mb_c[0], 1);
+            mbar_init(&mb_c[1], 1);
+            mbar_init(&mb_f, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0 && t0 < tile_end) coef_tma(cur, coefb, &mb_c[0]);
+    } else if (t0 < tile_end) {
+        prefetch_state(qin, cur, coefb);
+    }
+    if (t0 < tile_end) prefetch_geo(cur, geob);
     cp_async_commit();
     int n = 0;
     for (int t = t0; t < tile_end; t += step, ++n) {
         double* sc = coefb + (n & 1) * CT::COEF;
         const bool has_next = t + step < tile_end;
         const TI nxt = walk.next(cur);
-#if HGKS_CELL_ENDBAR
-        prefetch_faces(cur);
-        cp_async_commit();
-        if (has_next) prefetch_coef(nxt, coefb + ((n + 1) & 1) * CT::COEF, geob + ((n + 1) & 1) * CT::GEO);
-        cp_async_commit();
-#endif
         const int i0 = cur.i0, j = cur.j, k = cur.k;
         const long cbase = (long)(k + 1) * kp.S + (long)j * nx;
         const double* gg = geob + (n & 1) * CT::GEO;
         const long cglob_row = (long)nx * (j + (long)ny * (k + kp.kglob0));
         race_shake(kp, 2, n);
-#if HGKS_CELL_ENDBAR
-        cp_async_wait<2>();  // this tile's coefficients and widths
+        // this tile's coefficients and widths (issued a tile ahead)
+        if (tma) mbar_wait(&mb_c[n & 1], (n >> 1) & 1);
+        cp_async_wait<0>();
         __syncthreads();
-#else
-        // one barrier less per tile: the tile's faces and the next tile's
-        // coefficients are issued after this barrier, when every buffer the
-        // previous tile read is free
-        cp_async_wait<0>();  // this tile's coefficients and widths
-        __syncthreads();
-        prefetch_faces(cur);
+        // every buffer the previous tile read is free: the tile's faces (+
+        // stage 2's A), then the next tile's coefficients and widths
+        if (tma) {
+            if (tid == 0) {
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                if (!kp.report) faces_tma(cur);
+                if (has_next) coef_tma(nxt, coefb + ((n + 1) & 1) * CT::COEF, &mb_c[(n + 1) & 1]);
+            }
+        } else {
+            if (!kp.report) prefetch_faces(cur);
+            cp_async_commit();
+            if (has_next) prefetch_state(qin, nxt, coefb + ((n + 1) & 1) * CT::COEF);
+        }
+        if (has_next) prefetch_geo(nxt, geob + ((n + 1) & 1) * CT::GEO);
         cp_async_commit();
-        if (has_next) prefetch_coef(nxt, coefb + ((n + 1) & 1) * CT::COEF, geob + ((n + 1) & 1) * CT::GEO);
-        cp_async_commit();
-#endif
         const double hy = gg[2 * TC], hz = gg[2 * TC + 1];
         const double i2hy = gg[2 * TC + 2], i2hz = gg[2 * TC + 3];
 
@@ -982,7 +1039,21 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
         }
         if (kp.report) return;
         race_shake(kp, 3, n);
-        cp_async_wait<1>();  // this tile's face fluxes
+        // this tile's face fluxes (+ stage 2's A tile)
+        if (tma) {
+            mbar_wait(&mb_f, n & 1);
+            if (i0 + TC >= nx) {
+                // periodic x: the face at x = nx is face 0 (TMA has no wrap;
+                // that column arrived zero-filled)
+                const long rowk = (long)nx * (j + (long)ny * k);
+                for (int e = tid; e < CT::NFX * RW; e += NT) {
+                    const int rr = e, r0 = (rr / RW) * 10 + RO + rr % RW;
+                    fx[rr * XS + (nx - i0)] = f0[(long)r0 * kp.fs + rowk];
+                }
+            }
+        } else {
+            cp_async_wait<1>();
+        }
         __syncthreads();
 
         // ---- phase C: gather + projection + inverse mass (+ stage-2 combine)
@@ -1013,12 +1084,13 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
                     const int r = pf * RW + row - RO;
                     double Fm, Fp;
                     if (a == 0) {
-                        Fm = fx[r * (TC + 1) + l];
-                        Fp = fx[r * (TC + 1) + l + 1];
+                        Fm = fx[r * XS + l];
+                        Fp = fx[r * XS + l + 1];
                     } else {
                         const double* fa = a == 1 ? fy : fz;
-                        Fm = fa[r * 2 * TC + l];
-                        Fp = fa[r * 2 * TC + TC + l];
+                        const int hh = a == 1 ? CT::FYH : CT::FZH;
+                        Fm = fa[r * TC + l];
+                        Fp = fa[hh + r * TC + l];
                     }
                     const double Dm = Fm - Fp, Sm = Fm + Fp;
 #pragma unroll
@@ -1095,10 +1167,6 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
                 }
             }
         }
-#if HGKS_CELL_ENDBAR
-        race_shake(kp, 5, n);
-        __syncthreads();  // buffers of this tile are free for the next prefetch
-#endif
         cur = nxt;
     }
     cp_async_wait<0>();

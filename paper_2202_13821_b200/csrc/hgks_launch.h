@@ -13,8 +13,9 @@ struct KernelSet {
     // the y / z faces, {34, 1, NC} for the x faces — or null (cp.async staging)
     void (*face)(const KParams&, const double* q, const CUtensorMap* qmap, double* const f[3], cudaStream_t,
                  int report, const int* tile);
-    void (*cell)(const KParams&, int mode, const double* qin, double* const f[3], const double* qn,
-                 const double* L1, const double* Lt1, double* o0, double* o1, double* o2,
+    // cm: the launch's TMA tensor maps (KParams::cell_tma) or null
+    void (*cell)(const KParams&, const CellMaps* cm, int mode, const double* qin, double* const f[3],
+                 const double* qn, const double* L1, const double* Lt1, double* o0, double* o1, double* o2,
                  cudaStream_t, int report, const int* tile);
     // the same kernels restricted to owned z layers [kb, ke) (all three face
     // axes / the cell update of those layers), for the streamed host step
@@ -24,10 +25,11 @@ struct KernelSet {
     // multi-slab step that overlaps the halo exchange with interior faces
     void (*face_axis)(const KParams&, int axis, const double* q, const CUtensorMap* qmap, double* f,
                       cudaStream_t, int kb, int ke);
-    void (*cell_layers)(const KParams&, int mode, const double* qin, double* const f[3],
+    void (*cell_layers)(const KParams&, const CellMaps* cm, int mode, const double* qin, double* const f[3],
                         const double* qn, const double* L1, const double* Lt1, double* o0,
                         double* o1, double* o2, cudaStream_t, int kb, int ke);
     int face_tma;  // 1: the face kernels can stage by TMA (given qmap)
+    int cell_xs;   // x-face box width of the cell kernel (TC + 2)
     int face_smem[3];
     int cell_smem;
     int cell_tc;

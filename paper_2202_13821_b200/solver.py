@@ -472,6 +472,10 @@ class Solver:
         """Face-kernel staging: TMA boxes (default, even nx) or per-lane cp.async."""
         self.L.hgks_set_face_tma(self.h, int(on))
 
+    def set_cell_tma(self, on: bool = True):
+        """Cell-kernel staging: TMA boxes (default, even nx) or per-lane cp.async."""
+        self.L.hgks_set_cell_tma(self.h, int(on))
+
     def set_race_shake(self, seed: int):
         """Test hook: randomized per-warp delays before every cp.async wait and
         barrier of the persistent kernels (0 = off)."""

@@ -293,3 +293,27 @@ def test_race_shaker_bitwise(hgks, case, n, degree, cap):
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("case,n,degree,cap", [("tgv", 16, 2, 0), ("tgv", 8, 2, 3), ("tgv", 8, 3, 2),
+                                               ("adv3d", 12, 1, 2), ("vortex2d", 12, 3, 2), ("adv2d", 10, 2, 0)])
+def test_tma_and_cpasync_staging_bitwise(hgks, case, n, degree, cap):
+    """The face and cell kernels stage their tiles by TMA (tensor boxes +
+    mbarrier) or by per-lane cp.async; the staging moves the same values, so
+    residual, faces, host-dt steps and the device loop agree bit for bit
+    (including the periodic-x patch of the TMA paths and partial x tiles)."""
+    P = hgks
+    cfl = P.default_cfl(degree)
+    outs = []
+    for tma in (True, False):
+        r = P.setup_run(P.CaseConfig.named(case, n), P.RunOptions(degree=degree))
+        s = r.solver
+        s.set_grid_cap(cap)
+        s.set_face_tma(tma)
+        s.set_cell_tma(tma)
+        res = s.residual(s.compute_dt(cfl), faces=True)
+        s.step(s.compute_dt(cfl))
+        s.advance_records(1e9, cfl, max_steps=2)
+        outs.append([res["R"], res["Rt"], *res["faces"], s.get_state()[0]])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)

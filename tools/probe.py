@@ -13,6 +13,7 @@ print("setup", time.time() - t0)
 s = r.solver
 import os
 s.set_face_tma(os.environ.get("HGKS_FACE_TMA", "1") != "0")
+s.set_cell_tma(os.environ.get("HGKS_CELL_TMA", "1") != "0")
 s.set_kernel_timing(True)
 dt = s.compute_dt(0.15)
 print("dt", dt)
