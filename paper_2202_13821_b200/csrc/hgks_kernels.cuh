@@ -786,6 +786,8 @@ struct CellTile {
     static constexpr int GEO = 2 * TC + 4;               // widths of a tile: dx, 2/dx [TC]; dy, dz, 2/dy, 2/dz
     // stage 2: the tile's A = q + dt L1 + dt^2/6 Lt1 [NC][TC], prefetched with the faces
     static constexpr int AB = MODE == MODE_STAGE2 ? COEF : 0;
+    // projection items (cell, var, F|Ft); stage 2 projects only Ft
+    static constexpr int NITEMS = TC * 5 * (MODE == MODE_STAGE2 ? 1 : 2);
     static constexpr int SMEM = 2 * COEF + FX + FY + FZ + VF + LB + AB + pad16(2 * GEO);
     // bytes the face group of a tile lands (TMA transaction count)
     static constexpr unsigned FACE_TX =
@@ -838,6 +840,7 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
     if (kp.scal[SC_ACTIVE] == 0.0) return;  // halted device loop: no-op step
     const double dt = kp.scal[SC_DT];
     const bool tma = kp.cell_tma != 0;
+    constexpr int NITEMS = CT::NITEMS;
     const int tid = threadIdx.x;
     const int nx = kp.nx, ny = kp.ny;
     const int ntx = (nx + TC - 1) / TC;
@@ -1016,63 +1019,27 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
         const double hy = gg[2 * TC], hz = gg[2 * TC + 1];
         const double i2hy = gg[2 * TC + 2], i2hz = gg[2 * TC + 3];
 
-        // ---- phase B: smooth fluxes at volume points
-        for (int it = tid; it < TC * NVP; it += NT) {
-            const int l = it % TC;
-            const int p = SH::NQ == 2 ? it / TC : kVolOrder<P, DIM>.p[it / TC];
-            const int i = i0 + l;
-            if (i >= nx) continue;
-            const double i2h[3] = {gg[TC + l], i2hy, i2hz};
-            double e[20];
-            vol_eval_sym<P, DIM, TC>(p, sc + l, i2h, e);
-            double o[30];
-            double bad = 0.0;
-            const int rc = smooth_flux<VISC, NAX, MODE == MODE_STAGE2>(e, kp.gas, o, bad);
-            if (rc) {
-                report_error(kp, err_key(kp.stage, 1, cglob_row + i, p, 0, rc), bad);
-#pragma unroll
-                for (int m = 0; m < 30; ++m) o[m] = 0.0;
-            }
-#pragma unroll
-            for (int m = 0; m < 10 * NAX; ++m)
-                if (m % 10 >= RO) vf[(p * CT::VFW + (m / 10) * RW + m % 10 - RO) * TC + l] = o[m];
-        }
-        if (kp.report) return;
-        race_shake(kp, 3, n);
-        // this tile's face fluxes (+ stage 2's A tile)
-        if (tma) {
-            mbar_wait(&mb_f, n & 1);
+        // periodic x: the face at x = nx is face 0 (TMA has no wrap; that
+        // column arrived zero-filled), patched by threads [t0, t0 + nthr)
+        auto patch_x = [&](int t0p, int nthr) {
             if (i0 + TC >= nx) {
-                // periodic x: the face at x = nx is face 0 (TMA has no wrap;
-                // that column arrived zero-filled)
                 const long rowk = (long)nx * (j + (long)ny * k);
-                for (int e = tid; e < CT::NFX * RW; e += NT) {
-                    const int rr = e, r0 = (rr / RW) * 10 + RO + rr % RW;
-                    fx[rr * XS + (nx - i0)] = f0[(long)r0 * kp.fs + rowk];
+                for (int e = tid - t0p; e < CT::NFX * RW; e += nthr) {
+                    const int r0 = (e / RW) * 10 + RO + e % RW;
+                    fx[e * XS + (nx - i0)] = f0[(long)r0 * kp.fs + rowk];
                 }
             }
-        } else {
-            cp_async_wait<1>();
-        }
-        __syncthreads();
-
-        // ---- phase C: gather + projection + inverse mass (+ stage-2 combine)
-        constexpr int FT0 = MODE == MODE_STAGE2 ? 1 : 0;
-        constexpr int NITEMS = TC * 5 * (2 - FT0);
-        for (int it = tid; it < NITEMS; it += NT) {
+        };
+        // face part of projection item it (dg.hpp:404-425): + w jac B- F(minus
+        // face) - w jac B+ F(plus face), Legendre parity B+(p,n) = (-1)^{n_a} B-(p,n)
+        auto face_part = [&](int it, double* R) {
             const int l = it % TC, vv = it / TC;
-            const int v = vv % 5, ft = FT0 + vv / 5;  // ft: 0 -> F (R), 1 -> Ft (Rt)
-            const int i = i0 + l;
-            if (i >= nx) continue;
-            const double hx = gg[l];
-            const double i2h[3] = {gg[TC + l], i2hy, i2hz};
+            const int v = vv % 5, ft = (MODE == MODE_STAGE2 ? 1 : 0) + vv / 5;
             const int row = 5 * ft + v;
-            double R[N];
+            const double hx = gg[l];
+            const double jac[3] = {hy * hz * 0.25, hz * hx * 0.25, hx * hy * 0.25};
 #pragma unroll
             for (int m = 0; m < N; ++m) R[m] = 0.0;
-            // faces (dg.hpp:404-425): + w jac B- F(minus face) - w jac B+ F(plus face),
-            // with the Legendre parity B+(p,n) = (-1)^{n_a} B-(p,n)
-            const double jac[3] = {hy * hz * 0.25, hz * hx * 0.25, hx * hy * 0.25};
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const int nfp = a == 0 ? CT::NFX : a == 1 ? CT::NFY : CT::NFZ;
@@ -1103,6 +1070,52 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
 #pragma unroll
                 for (int m = 0; m < N; ++m) R[m] += jac[a] * acc[m];
             }
+        };
+
+        // ---- phase B: smooth fluxes at volume points
+        for (int it = tid; it < TC * NVP; it += NT) {
+            const int l = it % TC;
+            const int p = SH::NQ == 2 ? it / TC : kVolOrder<P, DIM>.p[it / TC];
+            const int i = i0 + l;
+            if (i >= nx) continue;
+            const double i2h[3] = {gg[TC + l], i2hy, i2hz};
+            double e[20];
+            vol_eval_sym<P, DIM, TC>(p, sc + l, i2h, e);
+            double o[30];
+            double bad = 0.0;
+            const int rc = smooth_flux<VISC, NAX, MODE == MODE_STAGE2>(e, kp.gas, o, bad);
+            if (rc) {
+                report_error(kp, err_key(kp.stage, 1, cglob_row + i, p, 0, rc), bad);
+#pragma unroll
+                for (int m = 0; m < 30; ++m) o[m] = 0.0;
+            }
+#pragma unroll
+            for (int m = 0; m < 10 * NAX; ++m)
+                if (m % 10 >= RO) vf[(p * CT::VFW + (m / 10) * RW + m % 10 - RO) * TC + l] = o[m];
+        }
+        if (kp.report) return;
+        race_shake(kp, 3, n);
+        // this tile's face fluxes (+ stage 2's A tile)
+        if (tma) {
+            mbar_wait(&mb_f, n & 1);
+            patch_x(0, NT);
+        } else {
+            cp_async_wait<1>();
+        }
+        __syncthreads();
+
+        // ---- phase C: gather + projection + inverse mass (+ stage-2 combine)
+        constexpr int FT0 = MODE == MODE_STAGE2 ? 1 : 0;
+        for (int it = tid; it < NITEMS; it += NT) {
+            const int l = it % TC, vv = it / TC;
+            const int v = vv % 5, ft = FT0 + vv / 5;  // ft: 0 -> F (R), 1 -> Ft (Rt)
+            const int i = i0 + l;
+            if (i >= nx) continue;
+            const double hx = gg[l];
+            const double i2h[3] = {gg[TC + l], i2hy, i2hz};
+            const int row = 5 * ft + v;
+            double R[N];
+            face_part(it, R);
             // volume (dg.hpp:427-448): + w (h0 h1 h2 / 8) (2/h_a) dB_a F_a
             const double vol = hx * hy * hz;
             const double vjac = vol * 0.125;
