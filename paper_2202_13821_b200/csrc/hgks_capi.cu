@@ -63,7 +63,7 @@ struct hgks_solver {
     std::vector<cudaEvent_t> ev_up, ev_c2, ev_dn;
     double* face[3] = {nullptr, nullptr, nullptr};
     // TMA tensor maps (x, row, comp) of buf[0], buf[1], qs for the TMA-staged
-    // face kernels (KernelSet::face_tma): [array][box 32 | box 34]
+    // face kernels (KernelSet::face_tma): [array][box 32 | x box HGKS_FACE_XBOX]
     CUtensorMap qmap[3][2];
     bool have_qmap = false;  // maps built (even nx)
     bool face_tma = true;    // use them (hgks_set_face_tma)
@@ -192,7 +192,7 @@ int make_qmaps(hgks_solver* s) {
         for (int b = 0; b < 2; ++b) {
             const cuuint64_t dims[3] = {(cuuint64_t)s->nx, (cuuint64_t)s->ny * (s->nzl + 2), (cuuint64_t)s->NC};
             const cuuint64_t strides[2] = {(cuuint64_t)s->nx * 8, (cuuint64_t)s->cs * 8};
-            const cuuint32_t box[3] = {b == 0 ? 32u : 34u, 1, (cuuint32_t)s->NC};
+            const cuuint32_t box[3] = {b == 0 ? 32u : (cuuint32_t)HGKS_FACE_XBOX, 1, (cuuint32_t)s->NC};
             const cuuint32_t estr[3] = {1, 1, 1};
             const CUresult r = encode(&s->qmap[a][b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, arrs[a], dims, strides, box,
                                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -52,6 +52,11 @@
 #ifndef HGKS_CELL_NT3
 #define HGKS_CELL_NT3 160
 #endif
+// stage-1 cell kernel of 3-D P1/P2 with 128 threads at 3 CTAs/SM and the
+// combine by lane-pair shuffles (1) or 160 threads at 2 CTAs/SM (0)
+#ifndef HGKS_CELL_S1X
+#define HGKS_CELL_S1X 0
+#endif
 // cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
 #ifndef HGKS_CELL_TC
 #define HGKS_CELL_TC 16
@@ -390,12 +395,18 @@ __device__ __forceinline__ void tma_load3(double* dst, const CUtensorMap* map, i
 // face-kernel stage layout: y / z faces [side][comp][32]; x faces one shared
 // [comp][34] row (x = i0-2 .. i0+31), minus side at column lane+1, plus side
 // at lane+2
+// x box width (build knob): 34 (x = i0-2 .. i0+31) or 48 (x = i0-16 ..
+// i0+31: the plus side's rows then start 128-byte aligned in shared memory)
+#ifndef HGKS_FACE_XBOX
+#define HGKS_FACE_XBOX 34
+#endif
 template <int NC, int AXIS>
 struct FaceStage {
+    static constexpr int XW = HGKS_FACE_XBOX, XOFF = XW - 32;  // x box: x = i0 - XOFF .. i0 + 31
     // stages start 128-byte aligned (TMA destinations)
-    static constexpr int STG = AXIS == 0 ? (34 * NC + 15) / 16 * 16 : 2 * NC * 32;
-    static constexpr int RSL = AXIS == 0 ? 34 : 32, RSR = RSL;
-    static constexpr int OFL = AXIS == 0 ? 1 : 0, OFR = AXIS == 0 ? 2 : NC * 32;
+    static constexpr int STG = AXIS == 0 ? (XW * NC + 15) / 16 * 16 : 2 * NC * 32;
+    static constexpr int RSL = AXIS == 0 ? XW : 32, RSR = RSL;
+    static constexpr int OFL = AXIS == 0 ? XOFF - 1 : 0, OFR = AXIS == 0 ? XOFF : NC * 32;
 };
 
 __device__ __forceinline__ void tma_load4(double* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
@@ -457,18 +468,19 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
     auto prefetch = [&](const TI& ti, double* dst) {
         constexpr int NW = NT / 32;
         if (AXIS == 0) {
-            // columns 0..33 = x = i0-2 .. i0+31 (periodic wrap at both ends;
-            // lanes 0, 1 also fetch columns 32, 33)
+            // column c = x = i0 - XOFF + c (periodic wrap at both ends); the
+            // kernel reads columns XOFF-1 .. XOFF+31: lanes fetch XOFF..XOFF+31,
+            // lane 0 also column XOFF-1
+            constexpr int XW = FaceStage<NC, AXIS>::XW, XOFF = FaceStage<NC, AXIS>::XOFF;
             const long row = (long)(ti.k + 1) * kp.S + (long)ti.j * nx;
-            auto xw = [&](int x) { return x < 0 ? x + nx : x >= nx ? x - nx : x; };
-            const int xa = ti.i0 - 2 + lane, xb = ti.i0 + 30 + lane;
-            const bool oka = xa < nx, okb = lane < 2 && xb < nx;
-            const double* sa = q + row + (oka ? xw(xa) : 0);
-            const double* sb = q + row + (okb ? xw(xb) : 0);
+            const int xa = ti.i0 + lane, xb = ti.i0 - 1;
+            const bool oka = xa < nx;
+            const double* sa = q + row + (oka ? xa : 0);
+            const double* sb = q + row + (xb < 0 ? xb + nx : xb);
 #pragma unroll 4
             for (int c = warp; c < NC; c += NW) {
-                cp_async8(dst + c * 34 + lane, sa + c * kp.cs, oka);
-                if (lane < 2) cp_async8(dst + c * 34 + 32 + lane, sb + c * kp.cs, okb);
+                cp_async8(dst + c * XW + XOFF + lane, sa + c * kp.cs, oka);
+                if (lane == 0) cp_async8(dst + c * XW + XOFF - 1, sb + c * kp.cs, true);
             }
             return;
         }
@@ -496,10 +508,10 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
         double* dst = smem + stage * STG;
         const int rowR = ti.j + ny * (ti.k + 1);
         if (AXIS == 0) {
-            // one 34-wide box from x = i0-2 (x < 0 at i0 = 0 is zero-filled
-            // and patched after the wait: TMA has no periodic wrap)
-            mbar_expect_tx(&mbar[stage], 34u * NC * 8u);
-            tma_load3(dst, &qmap, ti.i0 - 2, rowR, 0, &mbar[stage]);
+            // one XW-wide box from x = i0 - XOFF (x < 0 at i0 = 0 is
+            // zero-filled and patched after the wait: TMA has no periodic wrap)
+            mbar_expect_tx(&mbar[stage], (unsigned)FaceStage<NC, AXIS>::XW * NC * 8u);
+            tma_load3(dst, &qmap, ti.i0 - FaceStage<NC, AXIS>::XOFF, rowR, 0, &mbar[stage]);
             return;
         }
         const int rowL = AXIS == 1 ? (ti.j == 0 ? ny - 1 : ti.j - 1) + ny * (ti.k + 1) : ti.j + ny * ti.k;
@@ -523,6 +535,20 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
         if (t0 < tile_end) prefetch(cur, smem);
         cp_async_commit();
     }
+    // periodic x with TMA: the minus neighbour of face 0 is cell nx-1, which
+    // the box (x = -2 .. 31 at i0 = 0) cannot wrap to; its NC values are
+    // loaded into registers a tile ahead (latency hidden) and patched into
+    // column 1 after the box lands
+    double wrapv[2] = {0.0, 0.0};
+    auto load_wrap = [&](const TI& ti) {
+        if (AXIS == 0 && tma && ti.i0 == 0) {
+            const double* src = q + (long)(ti.k + 1) * kp.S + (long)ti.j * nx + (nx - 1);
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+                if (tid + r * NT < NC) wrapv[r] = __ldg(src + (long)(tid + r * NT) * kp.cs);
+        }
+    };
+    if (t0 < tile_end) load_wrap(cur);
     int n = 0;
     for (int t = t0; t < tile_end; t += step, ++n) {
         double* sc = smem + (HGKS_FACE_STAGES == 2 ? (n & 1) * STG : 0);
@@ -544,12 +570,13 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
         if (tma) {
             mbar_wait(&mbar[n & 1], (n >> 1) & 1);  // this tile's stage landed
             if (AXIS == 0 && i0 == 0) {
-                // periodic x: the minus neighbour of face 0 is cell nx-1 (TMA
-                // has no wrap; column 1 = x = -1 arrived zero-filled)
-                const double* src = q + (long)(k + 1) * kp.S + (long)j * nx + (nx - 1);
-                for (int c = tid; c < NC; c += NT) sc[c * 34 + 1] = __ldg(src + c * kp.cs);
+                // column 1 (x = -1) arrived zero-filled: the wrap values
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                    if (tid + r * NT < NC) sc[(tid + r * NT) * RSL + OFL] = wrapv[r];
                 __syncthreads();
             }
+            if (has_next) load_wrap(nxt);  // the next tile's, a tile ahead
         } else {
             if (HGKS_FACE_STAGES == 2) cp_async_wait<1>();  // this tile's stage
             else cp_async_wait<0>();
@@ -782,7 +809,11 @@ struct CellTile {
     static constexpr int FZ = pad16(2 * FZH);            // layers k, k+1 [half][pf][c][TC]
     static constexpr int VFW = 3 * RW;                   // flux rows per volume point
     static constexpr int VF = pad16(NVP * VFW * TC);     // volume-point fluxes [p][VFW][TC]
-    static constexpr int LB = MODE == MODE_STAGE1 ? pad16(2 * NC * TC) : 0;  // L, Lt of the tile (stage-1 q*)
+    // stage 1 of 3-D P1/P2 as one thread per (cell, volume point) at 3 CTAs
+    // per SM (HGKS_CELL_S1X): the F and Ft items of a (cell, var) sit in
+    // adjacent lanes and swap L1 / Lt1 by a shuffle, so no L, Lt tile
+    static constexpr bool S1X = HGKS_CELL_S1X && MODE == MODE_STAGE1 && P < 3 && DIM == 3;
+    static constexpr int LB = MODE == MODE_STAGE1 && !S1X ? pad16(2 * NC * TC) : 0;  // L, Lt of the tile (stage-1 q*)
     static constexpr int GEO = 2 * TC + 4;               // widths of a tile: dx, 2/dx [TC]; dy, dz, 2/dy, 2/dz
     // stage 2: the tile's A = q + dt L1 + dt^2/6 Lt1 [NC][TC], prefetched with the faces
     static constexpr int AB = MODE == MODE_STAGE2 ? COEF : 0;
@@ -795,8 +826,8 @@ struct CellTile {
     // threads / resident CTAs: stage 2 (half the tile, ~150 registers) runs
     // one thread per (cell, volume point) at 3 CTAs per SM for 3-D P1/P2
     static constexpr bool S2X = MODE == MODE_STAGE2 && P < 3 && DIM == 3;
-    static constexpr int NT = S2X ? TC * NVP : SH::NT_CELL;
-    static constexpr int MINB = S2X ? 3 : SH::MINB_CELL;
+    static constexpr int NT = S2X || S1X ? TC * NVP : SH::NT_CELL;
+    static constexpr int MINB = S2X || S1X ? 3 : SH::MINB_CELL;
 };
 
 // TMA tensor maps of one cell-kernel launch: the input state and stage 2's A
@@ -1033,8 +1064,16 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
         // face part of projection item it (dg.hpp:404-425): + w jac B- F(minus
         // face) - w jac B+ F(plus face), Legendre parity B+(p,n) = (-1)^{n_a} B-(p,n)
         auto face_part = [&](int it, double* R) {
-            const int l = it % TC, vv = it / TC;
-            const int v = vv % 5, ft = (MODE == MODE_STAGE2 ? 1 : 0) + vv / 5;
+            int l, v, ft;
+            if (CT::S1X) {
+                ft = it & 1;
+                l = (it >> 1) % TC;
+                v = (it >> 1) / TC;
+            } else {
+                l = it % TC;
+                v = (it / TC) % 5;
+                ft = (MODE == MODE_STAGE2 ? 1 : 0) + (it / TC) / 5;
+            }
             const int row = 5 * ft + v;
             const double hx = gg[l];
             const double jac[3] = {hy * hz * 0.25, hz * hx * 0.25, hx * hy * 0.25};
@@ -1107,10 +1146,18 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
         // ---- phase C: gather + projection + inverse mass (+ stage-2 combine)
         constexpr int FT0 = MODE == MODE_STAGE2 ? 1 : 0;
         for (int it = tid; it < NITEMS; it += NT) {
-            const int l = it % TC, vv = it / TC;
-            const int v = vv % 5, ft = FT0 + vv / 5;  // ft: 0 -> F (R), 1 -> Ft (Rt)
+            int l, v, ft;  // ft: 0 -> F (R), 1 -> Ft (Rt)
+            if (CT::S1X) {  // F / Ft of a (cell, var) in adjacent lanes
+                ft = it & 1;
+                l = (it >> 1) % TC;
+                v = (it >> 1) / TC;
+            } else {
+                l = it % TC;
+                v = (it / TC) % 5;
+                ft = FT0 + (it / TC) / 5;
+            }
             const int i = i0 + l;
-            if (i >= nx) continue;
+            if (!CT::S1X && i >= nx) continue;  // (S1X: every lane joins the shuffle; stores are predicated)
             const double hx = gg[l];
             const double i2h[3] = {gg[TC + l], i2hy, i2hz};
             const int row = 5 * ft + v;
@@ -1146,6 +1193,24 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
                 // mass_diag (dg.hpp:42-50): 1/M_n = (2nx+1)(2ny+1)(2nz+1)/vol (solver.hpp:49-51)
                 const double ivol = 1.0 / vol;
                 const double c6 = dt * dt / 6.0;
+                if (CT::S1X) {
+                    // the partner lane holds the other of (L1, Lt1):
+                    //   q* = q + dt/2 L1 + dt^2/8 Lt1 (F lane -> out0)
+                    //   A  = q + (dt L1 + dt^2/6 Lt1)  (Ft lane -> out1)
+                    const bool valid = i < nx;
+#pragma unroll
+                    for (int m = 0; m < N; ++m) {
+                        const double L = R[m] * (ctab<P, DIM>.massf[m] * ivol);
+                        const double Lo = __shfl_xor_sync(0xffffffffu, L, 1);
+                        const double q = sc[(m * 5 + v) * TC + l];
+                        const long gi = g0 + (long)(m * 5) * kp.cs;
+                        if (valid) {
+                            if (ft) out1[gi] = q + (dt * Lo + c6 * L);
+                            else out0[gi] = q + 0.5 * dt * L + 0.125 * dt * dt * Lo;
+                        }
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int m = 0; m < N; ++m) {
                     const double L = R[m] * (ctab<P, DIM>.massf[m] * ivol);
@@ -1160,7 +1225,7 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
                 }
             }
         }
-        if (MODE == MODE_STAGE1) {
+        if (MODE == MODE_STAGE1 && !CT::S1X) {
             // from shared memory, per coefficient (integrator.hpp:69-74):
             //   q* = q + dt/2 L1 + dt^2/8 Lt1           -> out0
             //   A  = q + (dt L1 + dt^2/6 Lt1)           -> out1 (stage 2 adds dt^2/6 * 2 Lt2)
