@@ -55,7 +55,7 @@
 // stage-1 cell kernel of 3-D P1/P2 with 128 threads at 3 CTAs/SM and the
 // combine by lane-pair shuffles (1) or 160 threads at 2 CTAs/SM (0)
 #ifndef HGKS_CELL_S1X
-#define HGKS_CELL_S1X 0
+#define HGKS_CELL_S1X 1
 #endif
 // cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
 #ifndef HGKS_CELL_TC
