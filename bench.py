@@ -62,7 +62,8 @@ def parse():
     ap.add_argument("--cfl", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=32, help="z-chunks of the streamed host-vector step")
+    ap.add_argument("--e2e-chunks", type=int, default=0,
+                    help="z-chunks of the streamed host-vector step (0: the library's choice, 48 at 128^3)")
     ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of CPU reference work")
     ap.add_argument("--face-staging", default="tma", choices=["tma", "cpasync"],
                     help="face-kernel staging: TMA boxes (default) or per-lane cp.async (A/B)")
@@ -313,7 +314,9 @@ def main():
             torch.distributed.all_reduce(t2, op=torch.distributed.ReduceOp.MAX)
         e2e = {"value": dof_glob * k2 / float(t2.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(s.ncoeffs * 8), "d2h_bytes_per_step": int(s.ncoeffs * 8),
-               "steps": k2, "path": f"hgks_two_stage_step_host_streamed (pinned host AoS state, {nch} z-chunks)"}
+               "steps": k2, "path": f"hgks_two_stage_step_host_streamed (pinned host AoS state, "
+                       f"{nch if nch > 0 else 'auto (48 at 128^3)'} z-chunks)",
+               "pcie_floor_ms": "17.65 ms for 839 MB each way at once (tools/pcie_probe.py, r02)"}
 
     if rank != 0:
         if world > 1:

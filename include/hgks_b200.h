@@ -99,7 +99,8 @@ int hgks_step(hgks_solver* s, double dt);
 int hgks_two_stage_step_host(hgks_solver* s, double* q, double dt);
 
 /* The same step with the host<->device traffic streamed: the z range is cut
- * into `nchunks` slabs whose uploads, face/cell kernels (a z-wavefront) and
+ * into `nchunks` slabs (<= 0: automatic, ~2.7 z layers each, at most 48)
+ * whose uploads, face/cell kernels (a z-wavefront) and
  * downloads overlap on three streams. Results are bitwise identical to
  * hgks_two_stage_step_host; on a state error q is restored to q^n (the
  * reference's two_stage_step leaves q untouched). Single slab only;

@@ -347,7 +347,7 @@ struct DeviceEval {
 };
 
 inline void two_stage_step(std::vector<double>& q, double dt, DeviceEval eval, TwoStageScratch&) {
-    eval.ws->dev->check(hgks_two_stage_step_host_streamed(eval.ws->dev->s, q.data(), dt, 16));
+    eval.ws->dev->check(hgks_two_stage_step_host_streamed(eval.ws->dev->s, q.data(), dt, 0));
 }
 
 // ---------------------------------------------------------- projection

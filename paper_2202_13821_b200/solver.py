@@ -281,7 +281,7 @@ class Solver:
             raise ConfigError("q must be a contiguous float64 vector of the state size")
         self._check(self.L.hgks_two_stage_step_host(self.h, _ptr(q), dt))
 
-    def two_stage_step_host_streamed(self, q: np.ndarray, dt: float, nchunks: int = 16):
+    def two_stage_step_host_streamed(self, q: np.ndarray, dt: float, nchunks: int = 0):
         """The host-vector step with H2D / compute / D2H overlapped over z chunks
         (bitwise identical results; on a state error q may be partially advanced)."""
         if not (q.dtype == np.float64 and q.flags["C_CONTIGUOUS"] and q.size == self.ncoeffs):
