@@ -317,8 +317,10 @@ HD TimeW time_weights_r(double tau, double inv_dt, double rh) {
     // branch-free: the general weights are formed and the tau = 0 limits
     // (flux.hpp:32-38) selected, so the face point stays one basic block
     TimeW w;
-    const double em = -expm1(-rh);
-    const double s = rh > 700.0 ? 1.0 : em;  // 1 - e^{-dt/(2 tau)}, clamp flux.hpp:40
+    // s = 1 - e^{-dt/(2 tau)}; for rh > 54 ln 2 = 37.43, e^{-rh} < 2^-54 and s
+    // rounds to 1 exactly (this also covers the reference's e^{-r} -> 0 clamp
+    // for r > 700, flux.hpp:40) — no expm1 on the chain at TGV 128^3 (rh ~ 38)
+    const double s = rh > 37.5 ? 1.0 : -expm1(-rh);
     const double x = tau * inv_dt;
     const double t3 = s * (2.0 + s);
     const double ss = s * s;
