@@ -4,8 +4,8 @@
 reads gpurun_out/launches.csv (gpu__time_duration per launch), the
 --set full reports gpurun_out/prof_face.ncu-rep / prof_cell.ncu-rep and
 gpurun_out/bench.json; writes profiles/<tag>_ncu_summary.md,
-profiles/<tag>_launches.csv and profiles/face_kernel_traffic.json (read by
-bench.py for roofline.traffic).
+profiles/<tag>_launches.csv (per-step DRAM traffic: tools/kernel_traffic.py ->
+profiles/kernel_traffic.json, read by bench.py for roofline.traffic / hbm).
 """
 import csv
 import json
@@ -197,11 +197,6 @@ def main(tag):
                    f"{ex['cell_stage2']['dadd']:.0f} DADD = {ex['cell_stage2']['fp64_flops']:.0f} flops"]
         md += [""]
     open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
-    if "face" in traffic:
-        t = traffic["face"]
-        json.dump({"tag": tag, "dram_bytes_per_launch": t["dram_bytes_per_launch"], "kernel": t["kernel"],
-                   "note": "one face_kernel launch (one axis); ncu --set full, cold cache"},
-                  open(os.path.join(PROF, "face_kernel_traffic.json"), "w"), indent=1)
     if bench:
         json.dump(bench, open(os.path.join(PROF, f"{tag}_bench.json"), "w"), indent=1)
     print("\n".join(md))
