@@ -76,6 +76,8 @@ def run_pair(P, O, case, n, degree, steps, grid_cap=0, nonuniform=False):
 
 
 @pytest.mark.parametrize("case,n,degree,steps", [
+    ("adv3d", 7, 2, 10),     # odd nx: no TMA view (16-byte strides), cp.async staging
+    ("tgv", 9, 3, 5),
     ("adv3d", 16, 2, 100),   # C1
     ("tgv", 32, 2, 20),      # multi-tile per CTA
     ("tgv", 32, 3, 10),      # P3: 3 points per face warp
