@@ -612,28 +612,33 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
             // block, so the scheduler can overlap their dependency chains; the
             // codes are checked afterwards in the reference's order
             // (left, right, merged state)
-            int rcs[3];
-            double bads[3];
+            int rc0 = 0, rc1 = 0, rc2 = 0;  // scalars, no runtime-indexed (local) arrays
+            double bad0 = 0.0, bad1 = 0.0, bad2 = 0.0;
+#ifdef HGKS_FACE_SIDE_ROLLED
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
             for (int side = 0; side < 2; ++side) {
                 double tr[20];
                 if (side == 0) face_trace_sym<P, DIM, AXIS, 0, RSL>(p, cL, i2hL, tr);
                 else face_trace_sym<P, DIM, AXIS, 1, RSR>(p, cR, i2hR, tr);
-                double ps = 0.0;
-                rcs[side] = flux_side<VISC>(tr, side, kp.gas, acc, ps, bads[side]);
+                double ps = 0.0, bd = 0.0;
+                const int rc = flux_side<VISC>(tr, side, kp.gas, acc, ps, bd);
+                if (side == 0) { rc0 = rc; bad0 = bd; } else { rc1 = rc; bad1 = bd; }
                 psum += ps;
             }
             {
                 // tau = mu / mean trace pressure (dg.hpp:378-383); dt/(2 tau) without a division
                 const double tau = VISC ? kp.two_mu / psum : 0.0;
                 const TimeW tw = time_weights_r(tau, inv_dt, VISC ? psum * rh_coef : 0.0);
-                rcs[2] = flux_merge<VISC>(kp.gas, tw, acc, F, Ft, bads[2]);
+                rc2 = flux_merge<VISC>(kp.gas, tw, acc, F, Ft, bad2);
             }
-            if (rcs[0] | rcs[1] | rcs[2]) {
-                // first failing stage, without runtime-indexed (local-memory) arrays
-                const int st = rcs[0] ? 0 : rcs[1] ? 1 : 2;
-                const int rc = rcs[0] ? rcs[0] : rcs[1] ? rcs[1] : rcs[2];
-                const double bd = rcs[0] ? bads[0] : rcs[1] ? bads[1] : bads[2];
+            if (rc0 | rc1 | rc2) {
+                // first failing stage in the reference's order (left, right, merged state)
+                const int st = rc0 ? 0 : rc1 ? 1 : 2;
+                const int rc = rc0 ? rc0 : rc1 ? rc1 : rc2;
+                const double bd = rc0 ? bad0 : rc1 ? bad1 : bad2;
                 if (owned) report_error(kp, err_key(kp.stage, 0, item, p, st, rc), bd);
                 fail = 1;
             }
