@@ -333,6 +333,55 @@ class Solver:
         s = self.error_norm_sums(case_name, t)
         return np.array([s[0], np.sqrt(s[1]), np.sqrt(s[2])])
 
+    def projection_points(self) -> np.ndarray:
+        """Physical coordinates [cell, p, 3] of the projection points of the
+        owned cells: x = center + h/2 * ref_p over the (k+2)^dim Gauss points,
+        (i, j, k) order with k fastest (dg.hpp:102-105, :193-220); z is 0 in 2-D."""
+        npts = self.L.hgks_projection_npts(self.h)
+        dim = self.scheme.dim
+        nq = int(round(npts ** (1.0 / dim)))
+        g = np.polynomial.legendre.leggauss(nq)[0]
+        if dim == 3:
+            ref = np.array([(g[a], g[b], g[c]) for a in range(nq) for b in range(nq) for c in range(nq)])
+        else:
+            ref = np.array([(g[a], g[b], 0.0) for a in range(nq) for b in range(nq)])
+        m = self.mesh
+        cx, hx = 0.5 * (m.xs[1:] + m.xs[:-1]), np.diff(m.xs)
+        cy, hy = 0.5 * (m.ys[1:] + m.ys[:-1]), np.diff(m.ys)
+        cz, hz = 0.5 * (m.zs[1:] + m.zs[:-1]), np.diff(m.zs)
+        ks = np.arange(self.z_begin, self.z_begin + self.z_count)
+        K, J, I = np.meshgrid(ks, np.arange(m.ny), np.arange(m.nx), indexing="ij")
+        I, J, K = I.ravel(), J.ravel(), K.ravel()   # owned cells, x fastest
+        pts = np.empty((I.size, npts, 3))
+        pts[:, :, 0] = cx[I, None] + 0.5 * hx[I, None] * ref[None, :, 0]
+        pts[:, :, 1] = cy[J, None] + 0.5 * hy[J, None] * ref[None, :, 1]
+        pts[:, :, 2] = cz[K, None] + 0.5 * hz[K, None] * ref[None, :, 2] if dim == 3 else 0.0
+        return pts
+
+    def _sample(self, field, rho_only: bool) -> np.ndarray:
+        pts = self.projection_points()
+        q = np.asarray(field(pts[..., 0], pts[..., 1], pts[..., 2]), dtype=np.float64)
+        if q.shape != (5,) + pts.shape[:2]:
+            raise ConfigError(f"field must return 5 conserved arrays shaped {pts.shape[:2]}, got {q.shape}")
+        return np.ascontiguousarray(q[0] if rho_only else np.moveaxis(q, 0, -1)).ravel()
+
+    def project_field(self, field, t: float = 0.0):
+        """project(field, mesh, tab, part) (dg.hpp:193-220) for a caller field:
+        field(x, y, z) -> (rho, rho U, rho V, rho W, E) arrays over the
+        projection points (numpy broadcasting); the quadrature sums run on the
+        device (hgks_project_samples)."""
+        smp = self._sample(field, False)
+        self._check(self.L.hgks_project_samples(self.h, _ptr(smp), t))
+
+    def error_norms_field(self, exact):
+        """error_norms(state, mesh, tab, exact, part) (dg.hpp:228-266) against a
+        caller field (its density): unreduced (L1, L2^2, cell-avg^2) sums, as
+        error_norm_sums."""
+        rho = self._sample(exact, True)
+        out = np.zeros(3)
+        self._check(self.L.hgks_error_norms_samples(self.h, _ptr(rho), _ptr(out)))
+        return out
+
     def tgv_diagnostics(self):
         """(Ek*vol, enstrophy*vol, vol) sums over owned cells (cases.hpp:165-204)."""
         e, z, v = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
