@@ -19,6 +19,8 @@ two_stage_step (integrator.hpp:64)     Solver.step / two_stage_step()
 advance (solver.hpp:62)                advance
 run_case (solver.hpp:110)              run_case
 tgv_diagnostics (cases.hpp:165)        Solver.tgv_diagnostics
+project(field, ...) (dg.hpp:193)       Solver.project_field / project_case
+error_norms (dg.hpp:228)               Solver.error_norms_field / run_error_norms
 dissipation_from_series (:208)         dissipation_from_series
 invalid_state_error (core.hpp:58)      InvalidStateError (+ .item/.phase)
 non_positive_dt (integrator.hpp:17)    NonPositiveDtError
