@@ -106,6 +106,26 @@ def test_c4_tgv128_parity(hgks, oracle_mod):
     assert ok
 
 
+
+@pytest.mark.parametrize("case,n,degree,steps", [
+    ("adv3d", 32, 2, 20),    # C2's mesh family, nonuniform widths at multi-tile size
+    ("adv3d", 16, 3, 10),
+    ("vortex2d", 80, 2, 20),  # 2-D mode with several tiles per CTA
+    ("adv2d", 64, 3, 10),
+])
+def test_nonuniform_and_2d_parity(hgks, oracle_mod, case, n, degree, steps):
+    """Nonuniform meshes (x = xi + 0.05 sin(pi xi), cases.hpp:50-57) and the
+    degenerate 2-D mode at sizes where the persistent CTAs walk several
+    tiles, against the reference itself (same dt sequence)."""
+    q_dev, q_ref, worst_dt, N = run_pair(hgks, oracle_mod, case, n, degree, steps,
+                                         nonuniform=case.startswith("adv"))
+    r = rel(q_dev, q_ref)
+    ok, pv = per_var_ok(q_dev, q_ref, N)
+    print(f"{case} P{degree} n={n} {steps} steps: global {r:.3e} per-var {pv:.3e} dt {worst_dt:.3e}")
+    assert worst_dt <= TOL_DT
+    assert r <= TOL_STATE
+    assert ok
+
 @pytest.mark.parametrize("case,n,degree,cap,nonuni", [
     ("tgv", 8, 2, 1, False),
     ("tgv", 8, 2, 7, False),
