@@ -60,6 +60,18 @@
 #define HGKS_CELL_S1X 1
 #endif
 // cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
+// P3 stage 2 (Ft only): each projection item split into two basis ranges
+// (one per warp of a pair) at 2 CTAs per SM; stage 1 keeps whole items at 1
+// CTA per SM (its split version spills at the 2-CTA register budget)
+#ifndef HGKS_CELL_P3_MINB2
+#define HGKS_CELL_P3_MINB2 2
+#endif
+#ifndef HGKS_CELL_P3_SPLIT2
+#define HGKS_CELL_P3_SPLIT2 1
+#endif
+#ifndef HGKS_CELL_P3_SPLIT1
+#define HGKS_CELL_P3_SPLIT1 0
+#endif
 #ifndef HGKS_CELL_TC
 #define HGKS_CELL_TC 16
 #endif
@@ -836,7 +848,9 @@ struct CellTile {
     // one thread per (cell, volume point) at 3 CTAs per SM for 3-D P1/P2
     static constexpr bool S2X = MODE == MODE_STAGE2 && P < 3 && DIM == 3;
     static constexpr int NT = S2X || S1X ? TC * NVP : SH::NT_CELL;
-    static constexpr int MINB = S2X || S1X ? 3 : SH::MINB_CELL;
+    static constexpr int MINB = S2X || S1X ? 3 : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_MINB2 : SH::MINB_CELL;
+    // P3: projection items split into two basis ranges (see HGKS_CELL_P3_SPLIT2)
+    static constexpr bool SPLIT = P == 3 && (MODE == MODE_STAGE2 ? HGKS_CELL_P3_SPLIT2 : HGKS_CELL_P3_SPLIT1);
 };
 
 // TMA tensor maps of one cell-kernel launch: the input state and stage 2's A
@@ -1241,7 +1255,20 @@ __global__ void __launch_bounds__(CellTile<P, DIM, MODE>::NT, CellTile<P, DIM, M
         // (S1X: 160 items on 128 threads, warp 0 takes the last 32; splitting
         // those 32 by basis range over the four warps measured slower:
         // stage 1 2.36 vs 2.22 ms)
-        for (int it = tid; it < NITEMS; it += NT) item_range(it, IC<0>{}, IC<N>{});
+        if constexpr (CT::SPLIT) {
+            // P3 stage 2: 40 items would leave most of the 7 warps idle; each
+            // item is split into two basis ranges [0, N/2) and [N/2, N), one
+            // per warp of a pair, so a warp's lanes share one range
+            const int w = tid >> 5, lane = tid & 31;
+            for (int base = (w >> 1) * 32; base < NITEMS; base += (NT / 64) * 32) {
+                const int it = base + lane;
+                if (it >= NITEMS || w >= (NT / 64) * 2) continue;
+                if (w & 1) item_range(it, IC<N / 2>{}, IC<N>{});
+                else item_range(it, IC<0>{}, IC<N / 2>{});
+            }
+        } else {
+            for (int it = tid; it < NITEMS; it += NT) item_range(it, IC<0>{}, IC<N>{});
+        }
         if (MODE == MODE_STAGE1 && !CT::S1X) {
             // from shared memory, per coefficient (integrator.hpp:69-74):
             //   q* = q + dt/2 L1 + dt^2/8 Lt1           -> out0
