@@ -63,6 +63,16 @@
 // P3 stage 2 (Ft only): each projection item split into two basis ranges
 // (one per warp of a pair) at 2 CTAs per SM; stage 1 keeps whole items at 1
 // CTA per SM (its split version spills at the 2-CTA register budget)
+// P3 cell tile: TC cells, NT threads, resident CTAs per SM (stage 1 / residual)
+#ifndef HGKS_CELL_P3_TC
+#define HGKS_CELL_P3_TC 8
+#endif
+#ifndef HGKS_CELL_P3_NT
+#define HGKS_CELL_P3_NT 224
+#endif
+#ifndef HGKS_CELL_P3_MINB
+#define HGKS_CELL_P3_MINB 1
+#endif
 #ifndef HGKS_CELL_P3_MINB2
 #define HGKS_CELL_P3_MINB2 2
 #endif
@@ -98,9 +108,9 @@ struct Shape {
     static constexpr int NAX = DIM == 3 ? 3 : 2;
     // cell tile along x and threads of the cell kernel (one thread per
     // (cell, volume point) in phase B for P1/P2)
-    static constexpr int TC = P == 3 ? 8 : HGKS_CELL_TC;
-    static constexpr int NT_CELL = P == 3 ? 224 : (DIM == 3 && HGKS_CELL_NT3 > 0) ? HGKS_CELL_NT3 : HGKS_CELL_TC * NVP;
-    static constexpr int MINB_CELL = P == 3 ? 1 : (HGKS_CELL_TC <= 16 ? 2 : 1);
+    static constexpr int TC = P == 3 ? HGKS_CELL_P3_TC : HGKS_CELL_TC;
+    static constexpr int NT_CELL = P == 3 ? HGKS_CELL_P3_NT : (DIM == 3 && HGKS_CELL_NT3 > 0) ? HGKS_CELL_NT3 : HGKS_CELL_TC * NVP;
+    static constexpr int MINB_CELL = P == 3 ? HGKS_CELL_P3_MINB : (HGKS_CELL_TC <= 16 ? 2 : 1);
 };
 
 enum : int { SC_DT = 0, SC_INV_DT = 1, SC_RH = 2, SC_ACTIVE = 3, SC_SLOT = 8 };
