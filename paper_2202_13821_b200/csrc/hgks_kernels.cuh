@@ -38,10 +38,20 @@
 #endif
 // P1/P2 face point as one basic block (both side passes + merge, codes
 // checked afterwards): TGV 9.36 -> 8.85 ms per step, adv3d 6.31 -> 6.04 (the
-// inviscid kernel still fits 3 CTAs/SM); P3 keeps the sequential passes
-// (measured 3% slower as one block)
+// inviscid kernel still fits 3 CTAs/SM); P3: see HGKS_FACE_P3_ONE_BLOCK (one block
+// only pays once the CTA has one point per warp)
 #ifndef HGKS_FACE_ONE_BLOCK
 #define HGKS_FACE_ONE_BLOCK 1
+#endif
+// P3 face CTAs: one point per warp (9-warp CTAs, 1 per SM, 168 registers
+// with ~130 B of spills) and the point as one basic block: TGV P3 64^3
+// 6.74 -> 5.91 ms per step against 3 points per warp in 3-warp CTAs (2 per
+// SM, 255 registers, 6 warps) with sequential side passes
+#ifndef HGKS_FACE_P3_PPW
+#define HGKS_FACE_P3_PPW 1
+#endif
+#ifndef HGKS_FACE_P3_ONE_BLOCK
+#define HGKS_FACE_P3_ONE_BLOCK 1
 #endif
 #ifndef HGKS_FACE_ACC_SMEM
 #define HGKS_FACE_ACC_SMEM 0
@@ -452,7 +462,7 @@ __device__ __forceinline__ void tma_load4(double* dst, const CUtensorMap* map, i
 template <int P, int DIM, int AXIS>
 struct FaceCTA {
     static constexpr int NFP = Shape<P, DIM>::template nfp<AXIS>();
-    static constexpr int PPW = (P == 3 && NFP % 3 == 0) ? 3 : 1;  // points per warp
+    static constexpr int PPW = (P == 3 && NFP % HGKS_FACE_P3_PPW == 0) ? HGKS_FACE_P3_PPW : 1;  // points per warp
     static constexpr int NT = 32 * NFP / PPW;
 };
 
@@ -629,7 +639,7 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
             int fail = 0;
             double psum = 0.0;  // p_l + p_r of the traces
             double F[5], Ft[5];
-            if constexpr (P < 3 && HGKS_FACE_ONE_BLOCK) {
+            if constexpr ((P < 3 || HGKS_FACE_P3_ONE_BLOCK) && HGKS_FACE_ONE_BLOCK) {
             // both side passes and the merge without early exits: one basic
             // block, so the scheduler can overlap their dependency chains; the
             // codes are checked afterwards in the reference's order
