@@ -69,19 +69,23 @@
 #ifndef HGKS_CELL_S1X
 #define HGKS_CELL_S1X 1
 #endif
-// cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
-// P3 stage 2 (Ft only): each projection item split into two basis ranges
-// (one per warp of a pair) at 2 CTAs per SM; stage 1 keeps whole items at 1
-// CTA per SM (its split version spills at the 2-CTA register budget)
-// P3 cell tile: TC cells, NT threads, resident CTAs per SM (stage 1 / residual)
+// P3 cell kernels (8-cell tiles, 27 volume points per cell): 6 warps at 2
+// CTAs per SM (≤ 168 registers, ~100 B of spills in stage 1), projection
+// items split into two basis ranges, one per warp of a pair (80 / 40 whole
+// items would leave most warps idle): TGV P3 64^3 5.89 -> 5.44 ms per step
+// against 7 warps at 1 CTA per SM with whole items. Per mode: stage 1 and
+// the residual (NT, MINB, SPLIT1), stage 2 (NT2, MINB2, SPLIT2).
 #ifndef HGKS_CELL_P3_TC
 #define HGKS_CELL_P3_TC 8
 #endif
 #ifndef HGKS_CELL_P3_NT
-#define HGKS_CELL_P3_NT 224
+#define HGKS_CELL_P3_NT 192
 #endif
 #ifndef HGKS_CELL_P3_MINB
-#define HGKS_CELL_P3_MINB 1
+#define HGKS_CELL_P3_MINB 2
+#endif
+#ifndef HGKS_CELL_P3_NT2
+#define HGKS_CELL_P3_NT2 192
 #endif
 #ifndef HGKS_CELL_P3_MINB2
 #define HGKS_CELL_P3_MINB2 2
@@ -90,8 +94,9 @@
 #define HGKS_CELL_P3_SPLIT2 1
 #endif
 #ifndef HGKS_CELL_P3_SPLIT1
-#define HGKS_CELL_P3_SPLIT1 0
+#define HGKS_CELL_P3_SPLIT1 1
 #endif
+// cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
 #ifndef HGKS_CELL_TC
 #define HGKS_CELL_TC 16
 #endif
@@ -867,7 +872,7 @@ struct CellTile {
     // threads / resident CTAs: stage 2 (half the tile, ~150 registers) runs
     // one thread per (cell, volume point) at 3 CTAs per SM for 3-D P1/P2
     static constexpr bool S2X = MODE == MODE_STAGE2 && P < 3 && DIM == 3;
-    static constexpr int NT = S2X || S1X ? TC * NVP : SH::NT_CELL;
+    static constexpr int NT = S2X || S1X ? TC * NVP : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_NT2 : SH::NT_CELL;
     static constexpr int MINB = S2X || S1X ? 3 : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_MINB2 : SH::MINB_CELL;
     // P3: projection items split into two basis ranges (see HGKS_CELL_P3_SPLIT2)
     static constexpr bool SPLIT = P == 3 && (MODE == MODE_STAGE2 ? HGKS_CELL_P3_SPLIT2 : HGKS_CELL_P3_SPLIT1);
