@@ -96,6 +96,10 @@
 #ifndef HGKS_CELL_P3_SPLIT1
 #define HGKS_CELL_P3_SPLIT1 1
 #endif
+// resident stage-2 CTAs per SM for 3-D P1/P2 (128 threads each)
+#ifndef HGKS_CELL_S2_MINB
+#define HGKS_CELL_S2_MINB 4
+#endif
 // cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
 #ifndef HGKS_CELL_TC
 #define HGKS_CELL_TC 16
@@ -873,7 +877,7 @@ struct CellTile {
     // one thread per (cell, volume point) at 3 CTAs per SM for 3-D P1/P2
     static constexpr bool S2X = MODE == MODE_STAGE2 && P < 3 && DIM == 3;
     static constexpr int NT = S2X || S1X ? TC * NVP : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_NT2 : SH::NT_CELL;
-    static constexpr int MINB = S2X || S1X ? 3 : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_MINB2 : SH::MINB_CELL;
+    static constexpr int MINB = S2X ? HGKS_CELL_S2_MINB : S1X ? 3 : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_MINB2 : SH::MINB_CELL;
     // P3: projection items split into two basis ranges (see HGKS_CELL_P3_SPLIT2)
     static constexpr bool SPLIT = P == 3 && (MODE == MODE_STAGE2 ? HGKS_CELL_P3_SPLIT2 : HGKS_CELL_P3_SPLIT1);
 };
