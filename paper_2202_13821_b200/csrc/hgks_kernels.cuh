@@ -27,10 +27,12 @@
 #ifndef HGKS_FACE_MINB
 #define HGKS_FACE_MINB 2
 #endif
-// P3 face CTAs have 9 warps: one CTA per SM keeps them spill-free
-#define HGKS_FACE_MINB_P(P) ((P) == 3 ? 1 : HGKS_FACE_MINB)
-// the inviscid flux fits 3 CTAs/SM without spills (166 registers)
-#define HGKS_FACE_MINB_PV(P, VISC) ((P) == 3 ? 1 : (VISC) ? HGKS_FACE_MINB : 3)
+// the inviscid flux fits 4 CTAs/SM (128 registers, no spills; 3 CTAs at 166
+// registers: adv3d P2 128^3 8.16 vs 8.08 ms per step); shared memory caps it at 4
+#ifndef HGKS_FACE_MINB_INV
+#define HGKS_FACE_MINB_INV 4
+#endif
+#define HGKS_FACE_MINB_PV(P, VISC) ((P) == 3 ? 1 : (VISC) ? HGKS_FACE_MINB : HGKS_FACE_MINB_INV)
 // face kernel staging buffers (2: double-buffered prefetch, 1: single) and
 // where the 35-double flux accumulator lives (0: registers, 1: shared memory)
 #ifndef HGKS_FACE_STAGES
