@@ -126,6 +126,18 @@ def test_nonuniform_and_2d_parity(hgks, oracle_mod, case, n, degree, steps):
     assert r <= TOL_STATE
     assert ok
 
+
+@pytest.mark.parametrize("case,n,degree", [("tgv", 4, 2), ("tgv", 4, 3), ("adv3d", 4, 3), ("adv2d", 4, 2),
+                                           ("vortex2d", 4, 3), ("tgv", 5, 2)])
+def test_smallest_mesh_parity(hgks, oracle_mod, case, n, degree):
+    """The smallest meshes build_mesh accepts (4 cells per axis,
+    cases.hpp:60): one partial x tile per row, x boxes wider than the mesh
+    (TMA zero fill + the periodic wrap patch), every CTA's tile its own
+    neighbour's."""
+    q_dev, q_ref, worst_dt, N = run_pair(hgks, oracle_mod, case, n, degree, 5)
+    assert worst_dt <= TOL_DT
+    assert rel(q_dev, q_ref) <= TOL_STATE
+
 @pytest.mark.parametrize("case,n,degree,cap,nonuni", [
     ("tgv", 8, 2, 1, False),
     ("tgv", 8, 2, 7, False),
