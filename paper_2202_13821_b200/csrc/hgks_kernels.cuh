@@ -21,11 +21,13 @@
 #include "hgks_ctables.cuh"
 #include "hgks_kinetics.cuh"
 
-// resident face CTAs per SM the register allocator must allow (build knob).
-// 2 (up to 255 registers, no spills) measured faster than 3 (168 registers,
-// ~700 B of spilled accumulators per thread): 11.6 vs 14.5 ms per step.
+// resident viscous face CTAs per SM the register allocator must allow. 3
+// (168 registers, ~110 B of spills, 12 warps/SM) against 2 (242 registers,
+// no spills, 8 warps): TGV P2 128^3 10.99 vs 11.15 ms per step, once the
+// point keeps its failure codes in scalars and the library erfc is out of
+// line (round 1, with ~700 B of spills, 3 measured 14.5 vs 11.6 ms)
 #ifndef HGKS_FACE_MINB
-#define HGKS_FACE_MINB 2
+#define HGKS_FACE_MINB 3
 #endif
 // the inviscid flux fits 4 CTAs/SM (128 registers, no spills; 3 CTAs at 166
 // registers: adv3d P2 128^3 8.16 vs 8.08 ms per step); shared memory caps it at 4

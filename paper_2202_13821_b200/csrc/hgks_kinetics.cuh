@@ -191,6 +191,16 @@ constexpr ErfSeries kErfSeries = make_erf_series();
 // 16-term series of erf (last term < 5e-18 relative, no cancellation:
 // erfc in (0.28, 1.72)) replaces the library's range-reduced rational + exp
 // chain; elsewhere the library erfc. Agrees with erfc to ~2 ulp.
+#ifndef HGKS_ERFC_NOINLINE
+#define HGKS_ERFC_NOINLINE 1
+#endif
+#if defined(__CUDA_ARCH__) && HGKS_ERFC_NOINLINE
+// the library erfc out of line: the slow path (|x| >= 0.75, supersonic
+// half-space moments) then costs no registers in the face point's one block
+__device__ __noinline__ double erfc_far(double x) { return erfc(x); }
+#else
+HD double erfc_far(double x) { return erfc(x); }
+#endif
 HD double erfc_near0(double x) {
     if (fabs(x) < 0.75) {
         const double z = x * x;
@@ -199,7 +209,7 @@ HD double erfc_near0(double x) {
         for (int n = 14; n >= 0; --n) s = fma(s, z, kErfSeries.a[n]);
         return 1.0 - (1.1283791670955125739 * x) * s;  // 2/sqrt(pi)
     }
-    return erfc(x);
+    return erfc_far(x);
 }
 
 // Half-space table for u>0 (sign=+1) or u<0 (sign=-1) (moments.hpp:35,43-46).
