@@ -104,7 +104,7 @@
 #ifndef HGKS_CELL_S2_MINB
 #define HGKS_CELL_S2_MINB 4
 #endif
-// cells per cell-kernel CTA for P1/P2 (16: 128 threads, 2 CTAs/SM)
+// cells per cell-kernel CTA for P1/P2 (16: 128 threads per CTA in stages 1 and 2)
 #ifndef HGKS_CELL_TC
 #define HGKS_CELL_TC 16
 #endif
@@ -469,9 +469,9 @@ __device__ __forceinline__ void tma_load4(double* dst, const CUtensorMap* map, i
 // along x (one lane each) at one (j, k), one face point per warp, so the
 // point index is warp-uniform. The two neighbour cells' coefficients of the
 // NEXT tile stream into the other half of a double-buffered shared-memory
-// stage [2][side][comp][32] (cp.async, coalesced 256 B rows) while the
-// current tile's fluxes are computed.
-// P3 (9 points) runs 3 points per warp so its 3-warp CTAs can hold 255 registers.
+// stage (TMA boxes, or cp.async rows when the state has no TMA view) while
+// the current tile's fluxes are computed. P3 (9 points) keeps one point per
+// warp by default (HGKS_FACE_P3_PPW; 3 gives 3-warp CTAs at 255 registers).
 template <int P, int DIM, int AXIS>
 struct FaceCTA {
     static constexpr int NFP = Shape<P, DIM>::template nfp<AXIS>();
