@@ -100,6 +100,17 @@
 #ifndef HGKS_CELL_P3_SPLIT1
 #define HGKS_CELL_P3_SPLIT1 1
 #endif
+// threads of the S1X stage-1 CTA: 160 = one per projection item (phase C in
+// one round; 32 idle in phase B), 15 warps/SM at 3 CTAs with ~170 B of
+// spills: stage 1 2.22 -> 2.19 ms (adv3d 1.86 -> 1.72) against 128 (one per
+// (cell, volume point)); 192: 3.48 ms, 160 at 2 CTAs/SM: 2.54 ms. P2 only:
+// P1 (4 basis functions, lighter phase C) stays at 128 (6.06 vs 6.33 ms)
+#ifndef HGKS_CELL_S1X_NT
+#define HGKS_CELL_S1X_NT 160
+#endif
+#ifndef HGKS_CELL_S1_MINB
+#define HGKS_CELL_S1_MINB 3
+#endif
 // resident stage-2 CTAs per SM for 3-D P1/P2 (128 threads each)
 #ifndef HGKS_CELL_S2_MINB
 #define HGKS_CELL_S2_MINB 4
@@ -880,8 +891,8 @@ struct CellTile {
     // threads / resident CTAs: stage 2 (half the tile, ~150 registers) runs
     // one thread per (cell, volume point) at 3 CTAs per SM for 3-D P1/P2
     static constexpr bool S2X = MODE == MODE_STAGE2 && P < 3 && DIM == 3;
-    static constexpr int NT = S2X || S1X ? TC * NVP : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_NT2 : SH::NT_CELL;
-    static constexpr int MINB = S2X ? HGKS_CELL_S2_MINB : S1X ? 3 : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_MINB2 : SH::MINB_CELL;
+    static constexpr int NT = S2X ? TC * NVP : S1X ? (P == 2 ? HGKS_CELL_S1X_NT : TC * NVP) : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_NT2 : SH::NT_CELL;
+    static constexpr int MINB = S2X ? HGKS_CELL_S2_MINB : S1X ? HGKS_CELL_S1_MINB : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_MINB2 : SH::MINB_CELL;
     // P3: projection items split into two basis ranges (see HGKS_CELL_P3_SPLIT2)
     static constexpr bool SPLIT = P == 3 && (MODE == MODE_STAGE2 ? HGKS_CELL_P3_SPLIT2 : HGKS_CELL_P3_SPLIT1);
 };
