@@ -115,6 +115,10 @@
 #ifndef HGKS_CELL_S2_MINB
 #define HGKS_CELL_S2_MINB 4
 #endif
+// P1 (20 coefficients per cell) fits 5 (96 registers): stage 2 2.85 -> 2.77 ms at 192^3
+#ifndef HGKS_CELL_S2_MINB_P1
+#define HGKS_CELL_S2_MINB_P1 5
+#endif
 // cells per cell-kernel CTA for P1/P2 (16: 128 threads per CTA in stages 1 and 2)
 #ifndef HGKS_CELL_TC
 #define HGKS_CELL_TC 16
@@ -892,7 +896,7 @@ struct CellTile {
     // one thread per (cell, volume point) at 3 CTAs per SM for 3-D P1/P2
     static constexpr bool S2X = MODE == MODE_STAGE2 && P < 3 && DIM == 3;
     static constexpr int NT = S2X ? TC * NVP : S1X ? (P == 2 ? HGKS_CELL_S1X_NT : TC * NVP) : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_NT2 : SH::NT_CELL;
-    static constexpr int MINB = S2X ? HGKS_CELL_S2_MINB : S1X ? HGKS_CELL_S1_MINB : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_MINB2 : SH::MINB_CELL;
+    static constexpr int MINB = S2X ? (P == 1 ? HGKS_CELL_S2_MINB_P1 : HGKS_CELL_S2_MINB) : S1X ? HGKS_CELL_S1_MINB : (P == 3 && MODE == MODE_STAGE2) ? HGKS_CELL_P3_MINB2 : SH::MINB_CELL;
     // P3: projection items split into two basis ranges (see HGKS_CELL_P3_SPLIT2)
     static constexpr bool SPLIT = P == 3 && (MODE == MODE_STAGE2 ? HGKS_CELL_P3_SPLIT2 : HGKS_CELL_P3_SPLIT1);
 };
