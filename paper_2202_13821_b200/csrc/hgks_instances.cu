@@ -70,8 +70,19 @@ struct Launch {
             grid = 1;
         }
         (void)NFP;
-        face_kernel<P, DIM, VISC, AXIS><<<grid, FaceCTA<P, DIM, AXIS>::NT, face_smem<AXIS>(), st>>>(
-            kp, q, f, first, count, map_or_null(qm ? qm + (AXIS == 0 ? 1 : 0) : nullptr));
+        launch_face<AXIS>(kp, grid, q, qm, f, first, count, st);
+    }
+    // stage-2 passes (kp.ft_only) run the Ft-only instantiation
+    template <int AXIS>
+    static void launch_face(const KParams& kp, int grid, const double* q, const CUtensorMap* qm, double* f,
+                            int first, int count, cudaStream_t st) {
+        const CUtensorMap m = map_or_null(qm ? qm + (AXIS == 0 ? 1 : 0) : nullptr);
+        if (kp.ft_only)
+            face_kernel<P, DIM, VISC, AXIS, true><<<grid, FaceCTA<P, DIM, AXIS>::NT, face_smem<AXIS>(), st>>>(
+                kp, q, f, first, count, m);
+        else
+            face_kernel<P, DIM, VISC, AXIS, false><<<grid, FaceCTA<P, DIM, AXIS>::NT, face_smem<AXIS>(), st>>>(
+                kp, q, f, first, count, m);
     }
     template <int AXIS>
     static void face_axis_layers(const KParams& kp, const double* q, const CUtensorMap* qm, double* f,
@@ -80,8 +91,7 @@ struct Launch {
         const int first = ntx * kp.ny * kb, count = ntx * kp.ny * (ke - kb);
         if (count <= 0) return;
         const int grid = std::min(count, capped(kp, face_grid[AXIS]));
-        face_kernel<P, DIM, VISC, AXIS><<<grid, FaceCTA<P, DIM, AXIS>::NT, face_smem<AXIS>(), st>>>(
-            kp, q, f, first, count, map_or_null(qm ? qm + (AXIS == 0 ? 1 : 0) : nullptr));
+        launch_face<AXIS>(kp, grid, q, qm, f, first, count, st);
     }
     static void face_axis_range(const KParams& kp, int axis, const double* q, const CUtensorMap* qm, double* f,
                                 cudaStream_t st, int kb, int ke) {
@@ -152,6 +162,9 @@ struct Launch {
         set((const void*)face_kernel<P, DIM, VISC, 0>, face_smem<0>());
         set((const void*)face_kernel<P, DIM, VISC, 1>, face_smem<1>());
         set((const void*)face_kernel<P, DIM, VISC, 2>, face_smem<2>());
+        set((const void*)face_kernel<P, DIM, VISC, 0, true>, face_smem<0>());
+        set((const void*)face_kernel<P, DIM, VISC, 1, true>, face_smem<1>());
+        set((const void*)face_kernel<P, DIM, VISC, 2, true>, face_smem<2>());
         set((const void*)cell_kernel<P, DIM, VISC, MODE_RESIDUAL>, cell_smem<MODE_RESIDUAL>());
         set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE1>, cell_smem<MODE_STAGE1>());
         set((const void*)cell_kernel<P, DIM, VISC, MODE_STAGE2>, cell_smem<MODE_STAGE2>());

@@ -494,7 +494,9 @@ struct FaceCTA {
     static constexpr int NT = 32 * NFP / PPW;
 };
 
-template <int P, int DIM, bool VISC, int AXIS>
+// FTO (the S2O4 second stage: only Ft is consumed) is a template argument so
+// the F-only arithmetic of the merge drops out of that instantiation
+template <int P, int DIM, bool VISC, int AXIS, bool FTO = false>
 __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P, VISC))
     face_kernel(KParams kp, const double* __restrict__ q, double* __restrict__ face,
                 int tile_first, int tile_count, const __grid_constant__ CUtensorMap qmap) {
@@ -744,7 +746,7 @@ __global__ void __launch_bounds__(FaceCTA<P, DIM, AXIS>::NT, HGKS_FACE_MINB_PV(P
                 Gt[1 + AXIS] = Ft[1];
                 Gt[1 + C1] = Ft[2];
                 Gt[1 + C2] = Ft[3];
-                if (!kp.ft_only) {
+                if (!FTO) {
 #pragma unroll
                     for (int v = 0; v < 5; ++v) out[v * kp.fs] = G[v];
                 }
