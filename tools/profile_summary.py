@@ -81,15 +81,30 @@ def exec_family(key):
         for r in rows:
             per[int(r[0])][r[12]] = num(r[14])
             per[int(r[0])]["kernel"] = r[4]
+        face_rows = []
         for idx in sorted(per):
             m = per[idx]
-            k = "face_point" if part == "face" else ("cell_stage" if ", 1>" in m["kernel"] else "cell_stage2")
             units = ncells * nfp if part == "face" else ncells
             e = {op: m.get(f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum", 0.0) / units
                  for op in ("dfma", "dmul", "dadd")}
             e["fp64_flops"] = 2 * e["dfma"] + e["dmul"] + e["dadd"]
             e["kernel"] = m["kernel"][:60]
-            out[k] = e
+            if part == "face":
+                face_rows.append(e)
+            else:
+                out["cell_stage" if ", 1>" in m["kernel"] else "cell_stage2"] = e
+        if face_rows:
+            # six launches = one step: stage 1 (x, y, z), stage 2 (Ft only); a
+            # single launch (older captures) is stage 1
+            def avg(rows):
+                r = {k: sum(x[k] for x in rows) / len(rows) for k in ("dfma", "dmul", "dadd", "fp64_flops")}
+                r["kernel"] = rows[0]["kernel"]
+                return r
+            out["face_point"] = avg(face_rows[:3])
+            if len(face_rows) >= 6:
+                out["face_point_stage2"] = avg(face_rows[3:6])
+                out["face_point_mean"] = {k: 0.5 * (out["face_point"][k] + out["face_point_stage2"][k])
+                                          for k in ("dfma", "dmul", "dadd", "fp64_flops")}
     if "cell_stage" in out and "cell_stage2" in out:
         out["cell_stage_mean"] = {k: 0.5 * (out["cell_stage"][k] + out["cell_stage2"][k])
                                   for k in ("dfma", "dmul", "dadd", "fp64_flops")}
