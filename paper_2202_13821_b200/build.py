@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 INC = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.environ.get("HGKS_LIB") or os.path.join(HERE, "libhgks_b200.so")
 OBJ = os.environ.get("HGKS_OBJ") or os.path.join(HERE, "_obj")
-# extra nvcc flags for kernel-variant experiments (e.g. -DHGKS_FACE_MINB=3)
+# extra nvcc flags for kernel-variant experiments (e.g. -DHGKS_FACE_MINB=2; tools/ab_lib.sh)
 EXTRA = os.environ.get("HGKS_NVCC_EXTRA", "").split()
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
