@@ -9,7 +9,8 @@ all-reduces of the dt bits and error keys, all inside the per-step CUDA graph
 of the device loop — except that the halo bytes move through NCCL's local
 path instead of NVLink and the all-reduces have one participant.
 
-usage: python tools/nccl_ring_timing.py [n] [steps]   -> one JSON line
+usage: python tools/nccl_ring_timing.py [n] [steps]   -> one JSON line (the last line
+of stdout: NCCL prints its version banner first)
 """
 import json
 import sys
